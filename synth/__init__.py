@@ -1,0 +1,142 @@
+"""Seeded synthetic workloads shared by the tests, bench.py and smoke().
+
+This module only DRAWS inputs (region lengths, CSR offsets, element values)
+and names the workload configurations of BASELINE.json; it contains none of
+the method's arithmetic (no filtering, no enumeration, no aggregation).  Both
+the oracle and the CUDA path consume the very same arrays produced here.
+
+Workload recipes:
+  D1 tiny   : R = 1000, lengths U{1..64}, int32 full range, 2 x HASH_LT(T=192), SUM_I64
+  D2 sweep  : region lengths fixed L or U{0..2L}, L in {1,4,32,256,4096};
+              int32 full range, 3 x HASH_LT(T=192), SUM_I64; fp32 variant
+              U[0,1) with SUM_F32.  Fixed-children reading N = 2^29 (the
+              paper's 512M integers).
+  D5 zipf   : lengths Zipf(s=1.2) on [1, 4096], int32, sweep filters, SUM_I64.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+# Odd multipliers for the HASH_LT filters (reading A13 of SURVEY §8(c)).
+HASH_A = (0x9E3779B1, 0x85EBCA6B, 0xC2B2AE35, 0x27D4EB2F)
+HASH_T = 192                      # keep ~3/4 per stage
+
+
+def sweep_stages(n: int = 3, T: int = HASH_T):
+    return [("hash_lt", HASH_A[k], T) for k in range(n)]
+
+
+def tiny_stages():
+    return sweep_stages(2)
+
+
+# ----------------------------------------------------------------- numpy side
+def _rng(seed: int) -> np.random.Generator:
+    return np.random.Generator(np.random.PCG64(seed))
+
+
+def lengths(R: int, dist: str, L: int = 0, seed: int = 0, lo: int = 0, hi: int = 0,
+            zipf_s: float = 1.2, zipf_max: int = 4096) -> np.ndarray:
+    """Region lengths (int64[R]).
+    dist: "fixed" (all L) | "var" (U{0..2L}, mean L; the paper's
+    uniform-in-[0,max] with max = 2L) | "uniform" (U{lo..hi}) |
+    "zipf" (P(k) ~ k^-s on [1, zipf_max])."""
+    g = _rng(seed)
+    if dist == "fixed":
+        return np.full(R, L, np.int64)
+    if dist == "var":
+        return g.integers(0, 2 * L, size=R, endpoint=True, dtype=np.int64)
+    if dist == "uniform":
+        return g.integers(lo, hi, size=R, endpoint=True, dtype=np.int64)
+    if dist == "zipf":
+        k = np.arange(1, zipf_max + 1, dtype=np.float64)
+        cdf = np.cumsum(k ** -zipf_s)
+        cdf /= cdf[-1]
+        u = g.random(R)
+        return (np.searchsorted(cdf, u, side="right") + 1).clip(1, zipf_max).astype(np.int64)
+    raise ValueError(dist)
+
+
+def offsets(lens: np.ndarray, base: int = 0) -> np.ndarray:
+    """CSR offsets int64[R+1] with offsets[0] = base."""
+    off = np.empty(lens.size + 1, np.int64)
+    off[0] = base
+    np.cumsum(lens, out=off[1:])
+    off[1:] += base
+    return off
+
+
+def values(N: int, dtype: str, seed: int = 0) -> np.ndarray:
+    """Element values: i32/u32 full range, f32 U[0,1), u8 full range."""
+    g = _rng(seed)
+    if dtype == "i32":
+        return g.integers(-2**31, 2**31, size=N, dtype=np.int64).astype(np.int32)
+    if dtype == "u32":
+        return g.integers(0, 2**32, size=N, dtype=np.uint64).astype(np.uint32)
+    if dtype == "f32":
+        return g.random(N, dtype=np.float32)
+    if dtype == "u8":
+        return g.integers(0, 256, size=N, dtype=np.uint8)
+    raise ValueError(dtype)
+
+
+def tiny(seed: int = 0x5EED + 1):
+    """D1: 1000 parents, 1-64 children each, int32, 2 int filters, SUM_I64."""
+    lens = lengths(1000, "uniform", lo=1, hi=64, seed=seed)
+    off = offsets(lens)
+    return values(int(off[-1]), "i32", seed + 17), off, tiny_stages(), "sum_i64"
+
+
+# ----------------------------------------------------------------- torch side
+def torch_lengths(R: int, dist: str, L: int = 0, seed: int = 0, device="cuda",
+                  zipf_s: float = 1.2, zipf_max: int = 4096, lo: int = 0, hi: int = 0):
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    if dist == "fixed":
+        return torch.full((R,), L, dtype=torch.int64, device=device)
+    if dist == "var":
+        return torch.randint(0, 2 * L + 1, (R,), generator=g, device=device, dtype=torch.int64)
+    if dist == "uniform":
+        return torch.randint(lo, hi + 1, (R,), generator=g, device=device, dtype=torch.int64)
+    if dist == "zipf":
+        k = torch.arange(1, zipf_max + 1, dtype=torch.float64, device=device)
+        cdf = torch.cumsum(k ** -zipf_s, 0)
+        cdf /= cdf[-1].clone()
+        u = torch.rand(R, generator=g, device=device, dtype=torch.float64)
+        return (torch.searchsorted(cdf, u, right=True) + 1).clamp(1, zipf_max).to(torch.int64)
+    raise ValueError(dist)
+
+
+def torch_offsets(lens, base: int = 0):
+    import torch
+    off = torch.empty(lens.numel() + 1, dtype=torch.int64, device=lens.device)
+    off[0] = base
+    torch.cumsum(lens, 0, out=off[1:])
+    if base:
+        off[1:] += base
+    return off
+
+
+def torch_values(N: int, dtype: str, seed: int = 0, device="cuda"):
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    if dtype == "i32":
+        return torch.randint(-2**31, 2**31, (N,), generator=g, device=device, dtype=torch.int64).to(torch.int32) \
+            if N <= 2**24 else _torch_bits(N, g, device).view(torch.int32)
+    if dtype == "u32":
+        return _torch_bits(N, g, device).view(torch.int32)        # raw bits; reinterpret as u32
+    if dtype == "f32":
+        return torch.rand(N, generator=g, device=device, dtype=torch.float32)
+    if dtype == "u8":
+        return torch.randint(0, 256, (N,), generator=g, device=device, dtype=torch.uint8)
+    raise ValueError(dtype)
+
+
+def _torch_bits(N: int, g, device):
+    import torch
+    # 32 random bits per element from two 16-bit draws (int32 randint range limits)
+    hi = torch.randint(0, 1 << 16, (N,), generator=g, device=device, dtype=torch.int32)
+    lo = torch.randint(0, 1 << 16, (N,), generator=g, device=device, dtype=torch.int32)
+    return (hi << 16) | lo
