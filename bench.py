@@ -1,0 +1,441 @@
+"""bench.py — throughput of the region-streaming hot path (BASELINE.json metric:
+"input items/sec and SIMD lane occupancy vs region length, signal vs tagged,
+1-8 B200").
+
+Default (N=1): BASELINE configs[1], region-length sweep, in the fixed-children
+reading of SURVEY §8(d): N = 2^29 int32 children (the paper's 512M integers,
+P:565-567), fixed region length L = 4096 (R = 131072), 3 HASH_LT filters,
+SUM_I64, signal strategy.  A "step" is one rs_pipeline_run over that batch
+(enumerate -> 3 filters -> aggregate, all §8(a) rows).  Inputs (2 GB) exceed
+the 126 MB L2, so no flush is needed between steps.
+
+--impl reference times the CPU oracle (the paper-derived interpreter) on the
+host cores instead (the tier's reference arm).
+Under torchrun (N>1) every rank runs its own shard (whole regions, weak
+scaling) and the per-region aggregates are gathered to rank 0 with NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "input items/sec and SIMD lane occupancy vs region length, signal vs tagged, 1-8 B200"
+FALLBACK_HBM_GBS = 6650.0        # /opt/skills/guides/B200_PROFILING.md fallback ("of fallback")
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            d = json.load(open(p))
+            for k in ("hbm_gbs", "hbm_GBps", "hbm"):
+                if k in d:
+                    v = d[k]
+                    return float(v["value"] if isinstance(v, dict) else v), "measured"
+        except Exception:
+            pass
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu_index=0):
+        self.samples = []
+        self.proc = None
+        self.gpu = gpu_index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for n, v in zip(names, s[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------ workloads
+def workload_spec(name):
+    import synth
+    if name == "sweep_fixed_L4096":
+        return dict(N=1 << 29, dist="fixed", L=4096, stages=synth.sweep_stages(3), agg="sum_i64", dtype="i32")
+    if name.startswith("sweep_"):
+        # sweep_<fixed|var>_L<L>
+        _, dist, l = name.split("_")
+        return dict(N=1 << 29, dist=dist, L=int(l[1:]), stages=synth.sweep_stages(3), agg="sum_i64", dtype="i32")
+    if name == "zipf":
+        return dict(N=1 << 30, dist="zipf", L=0, stages=synth.sweep_stages(3), agg="sum_i64", dtype="i32")
+    raise ValueError(name)
+
+
+def make_inputs(spec, seed, device):
+    import synth
+    import torch
+    N, dist, L = spec["N"], spec["dist"], spec["L"]
+    if dist == "fixed":
+        lens = torch.full((N // L,), L, dtype=torch.int64, device=device)
+    elif dist == "var":
+        lens = synth.torch_lengths(N // L, "var", L=L, seed=seed, device=device)
+    else:
+        lens = synth.torch_lengths(int(N / 208.7), "zipf", seed=seed, device=device)
+    off = synth.torch_offsets(lens)
+    n = int(off[-1].item())
+    vals = synth.torch_values(n, spec["dtype"], seed=seed + 1, device=device)
+    return vals, off
+
+
+def alg_bytes(n, R, agg):
+    out_b = {"sum_i64": 8, "sum_f32": 4, "count_min_u32": 8, "count_xor64": 16}[agg]
+    return 4 * n + 8 * (R + 1) + out_b * R
+
+
+# ------------------------------------------------------------------- oracle
+def oracle_rate(vals_h, off_h, stages, agg, budget_s=10.0, cores=None):
+    """Time the CPU oracle's pipeline interpreter (as it stands) on a bounded
+    prefix sample of the workload, sharded over host cores by whole regions
+    (regions are independent contexts; ctypes releases the GIL)."""
+    import concurrent.futures as cf
+
+    import oracle
+    cores = cores or len(os.sched_getaffinity(0))
+    R = off_h.size - 1
+    # calibrate on a small sample to size a ~budget_s run
+    r_small = min(R, max(1, int(np.searchsorted(off_h, off_h[0] + (1 << 18)))))
+    t0 = time.perf_counter()
+    oracle.interp(vals_h, off_h[:r_small + 1], stages, agg, check=False)
+    dt = time.perf_counter() - t0
+    n_small = int(off_h[r_small] - off_h[0])
+    per_item = dt / max(1, n_small)
+    target = int(budget_s * cores / max(per_item, 1e-12))
+    r_end = int(min(R, max(cores, np.searchsorted(off_h, off_h[0] + target))))
+    bounds = np.linspace(0, r_end, cores + 1).astype(np.int64)
+
+    def work(i):
+        a, b = int(bounds[i]), int(bounds[i + 1])
+        if b > a:
+            oracle.interp(vals_h, off_h[a:b + 1], stages, agg, check=False)
+        return int(off_h[b] - off_h[a])
+
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(cores) as ex:
+        items = sum(ex.map(work, range(cores)))
+    wall = time.perf_counter() - t0
+    return items / wall, cores, f"interpreter on regions [0,{r_end}) = {items} children, {cores} threads, {wall:.1f}s"
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on this box's cores (tier reference arm)."""
+    import synth
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    spec = workload_spec(args.workload)
+    g = np.random.default_rng(0)
+    # host-side sample of the same workload shape
+    n_s = 1 << 24
+    if spec["dist"] == "fixed":
+        lens = np.full(n_s // spec["L"], spec["L"], np.int64)
+    elif spec["dist"] == "var":
+        lens = synth.lengths(n_s // spec["L"], "var", L=spec["L"], seed=1)
+    else:
+        lens = synth.lengths(int(n_s / 208.7), "zipf", seed=1)
+    off = synth.offsets(lens)
+    vals = synth.values(int(off[-1]), spec["dtype"], seed=2)
+    rates = []
+    desc = None
+    cores = None
+    for i in range(args.warmup + args.steps):
+        r, cores, desc = oracle_rate(vals, off, spec["stages"], spec["agg"], budget_s=max(1.0, 20.0 / max(1, args.steps)))
+        if i >= args.warmup:
+            rates.append(r)
+    v = statistics.median(rates)
+    line = {"metric": METRIC, "value": v, "unit": "items/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32->int64", "data": "synthetic",
+            "config": {"workload": args.workload, "strategy": "signal", "w": 128},
+            "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "items/s", "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": v, "unit": "items/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------- GPU arm
+def traffic_for(workload, strategy):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get(f"{workload}:{strategy}")
+        except Exception:
+            return None
+    return None
+
+
+def time_pipeline(p, vals, off, out, ws, steps, warmup, torch):
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        p.run(vals, off, out, ws)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    main_ms = []
+    for a, b in ev:
+        a.record(stream)
+        p.run(vals, off, out, ws)
+        b.record(stream)
+        main_ms.append(p.kernel_times()[1])
+    torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    return step_ms, main_ms
+
+
+def lane_stats(st):
+    res = []
+    for n in range(1, st.shape[0]):
+        d, f, it, s = (int(x) for x in st[n])
+        res.append({"lane_fraction": (it / (128 * d)) if d else None, "full_rate": (f / d) if d else None,
+                    "ensembles": d, "items": it, "signals": s})
+    return res
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2006_07478_b200 as rs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    spec = workload_spec(args.workload)
+    vals, off = make_inputs(spec, seed=0x5EED + 2 + 1000 * rank, device=dev)
+    n = int(vals.numel())
+    R = int(off.numel() - 1)
+    flags = rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING
+    p = rs.Pipeline(spec["stages"], spec["agg"], strategy=args.strategy, flags=flags)
+    out = p.alloc_outputs(R, dev)
+    ws = p.alloc_workspace(R, n, dev)
+    gather_buf = None
+    if world > 1 and rank == 0:
+        gather_buf = [torch.empty_like(out[0]) for _ in range(world)]
+
+    # ---- device-timed region: W warm-ups, then K steps, barrier + sync both sides
+    for _ in range(args.warmup):
+        p.run(vals, off, out, ws)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    main_ms = []
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for _ in range(args.steps):
+            p.run(vals, off, out, ws)
+            if world > 1:
+                dist.gather(out[0], gather_buf if rank == 0 else None, dst=0)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    total_ms = t0.elapsed_time(t1)
+    # per-launch main-kernel time, measured live with events on the launching stream
+    for _ in range(max(3, min(args.steps, 10))):
+        p.run(vals, off, out, ws)
+        main_ms.append(p.kernel_times()[1])
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    code = p.check()
+    st = p.stats()
+    ms_step = total_ms / args.steps
+    value = n * world / (ms_step / 1e3)
+    main_avg = statistics.mean(main_ms)
+    bytes_alg = alg_bytes(n, R, spec["agg"])
+    peak, peak_kind = hbm_peak()
+    achieved = bytes_alg / (main_avg / 1e3) / 1e9
+
+    # ---- end-to-end through the C ABI with host buffers (pinned), every step
+    e2e = None
+    if not args.no_e2e:
+        vh = torch.empty(vals.shape, dtype=vals.dtype, pin_memory=True)
+        vh.copy_(vals)
+        oh = torch.empty(off.shape, dtype=off.dtype, pin_memory=True)
+        oh.copy_(off)
+        outh = torch.empty(out[0].shape, dtype=out[0].dtype, pin_memory=True)
+        p.run_host(vh, oh, outh)          # warm-up (device buffers allocated here)
+        k = max(1, min(args.steps, 3))
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(k):
+            p.run_host(vh, oh, outh)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = a.elapsed_time(b) / k
+        e2e = {"value": n * world / (e2e_ms / 1e3), "unit": "items/s",
+               "h2d_bytes_per_step": int(vals.numel() * vals.element_size() + off.numel() * 8),
+               "d2h_bytes_per_step": int(out[0].numel() * out[0].element_size()), "ms_per_step": e2e_ms}
+        ok = torch.equal(outh, out[0].cpu())
+        if not ok:
+            e2e["mismatch"] = True
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only), bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        n_s = min(n, 1 << 24)
+        r_s = int(torch.searchsorted(off, off[0] + n_s).item())
+        vh = vals[: int(off[r_s].item())].cpu().numpy()
+        oh = off[: r_s + 1].cpu().numpy()
+        rate, cores, desc = oracle_rate(vh, oh, spec["stages"], spec["agg"], budget_s=10.0)
+        cpu = {"value": rate, "unit": "items/s", "cores": cores, "kind": "oracle", "sample": desc}
+
+    sweep = None
+    if args.sweep and rank == 0:
+        sweep = run_sweep(rs, torch, dev, args)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "items/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32->int64", "data": "synthetic",
+            "config": {"workload": args.workload, "children": n * world, "regions": R * world,
+                       "strategy": args.strategy, "w": 128, "stages": len(spec["stages"]),
+                       "l2": "inputs (2 GiB) larger than L2; no flush", "parallelism": f"regions x{world}"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic_for(args.workload, args.strategy),
+                         "peak_kind": peak_kind, "kernel": "k_pipeline", "kernel_ms": main_avg,
+                         "algorithmic_bytes": bytes_alg},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": p.launches() * args.steps,
+            "clocks": clk.summary(),
+            "occupancy": lane_stats(st),
+            "device_error": code,
+        }
+        if sweep is not None:
+            line["sweep"] = sweep
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_sweep(rs, torch, dev, args):
+    """Items/s and per-node lane fraction vs region length, signal vs tagged
+    (BASELINE metric; Figs. 5-6 shape).  N = 2^29 children per point."""
+    res = []
+    Ls = [int(x) for x in args.sweep_L.split(",")]
+    import synth
+    N = 1 << 29
+    vals = synth.torch_values(N, "i32", seed=11, device=dev)
+    for dist_ in ("fixed", "var"):
+        for L in Ls:
+            if dist_ == "fixed":
+                lens = torch.full((N // L,), L, dtype=torch.int64, device=dev)
+            else:
+                lens = synth.torch_lengths(N // L, "var", L=L, seed=L, device=dev)
+                # keep the children count <= N
+                cs = torch.cumsum(lens, 0)
+                lens = lens[: int(torch.searchsorted(cs, N, right=True).item())]
+            off = synth.torch_offsets(lens)
+            n = int(off[-1].item())
+            R = off.numel() - 1
+            for strat in ("signal", "tagged"):
+                p = rs.Pipeline(synth.sweep_stages(3), "sum_i64", strategy=strat,
+                                flags=rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING)
+                out = p.alloc_outputs(R, dev)
+                ws = p.alloc_workspace(R, n, dev)
+                p.run(vals, off, out, ws)
+                torch.cuda.synchronize()
+                ms = []
+                for _ in range(args.sweep_reps):
+                    p.run(vals, off, out, ws)
+                    ms.append(sum(p.kernel_times()))
+                st = p.stats()
+                t = statistics.median(ms)
+                res.append({"dist": dist_, "L": L, "strategy": strat, "children": n, "regions": R,
+                            "ms": t, "items_per_s": n / (t / 1e3),
+                            "hbm_frac": alg_bytes(n, R, "sum_i64") / (t / 1e3) / 1e9 / hbm_peak()[0],
+                            "lane_fraction": [x["lane_fraction"] for x in lane_stats(st)],
+                            "full_rate": [x["full_rate"] for x in lane_stats(st)],
+                            "error": p.check()})
+                del out, ws
+            del off, lens
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="sweep_fixed_L4096")
+    ap.add_argument("--strategy", default="signal", choices=["signal", "tagged"])
+    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--sweep-L", default="1,4,32,256,4096")
+    ap.add_argument("--sweep-reps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,196 @@
+/*
+ * rs.h — C ABI of the B200-native region-based streaming library.
+ *
+ * Implements the data-parallel hot path of Timcheck & Buhler, "Streaming
+ * Computations with Region-Based State on SIMD Architectures" (arXiv
+ * 2006.07478).  Citations "P:a-b" are lines of the paper's PAPER.md with the
+ * section they fall in; design readings are DESIGN.md §3 (A1-A26).
+ *
+ * What a call computes (§4, Fig. 3-5): a stream of
+ * composite parent objects ("regions"), each holding 0+ elements, is
+ * ENUMERATED into the stream of its elements, passed
+ * through FILTER / TRANSFORM stages that keep or drop each item (P:109-118
+ * §2.1, Fig. 5 `if (isGood(v)) push(...)` P:529), and AGGREGATED to exactly
+ * one result per parent (Fig. 5 begin/run/end P:532-534).
+ * Region boundaries reach every stage either as credit-counted Begin/End
+ * signals (RS_STRATEGY_SIGNAL: §3) or as a region tag carried by
+ * every item (RS_STRATEGY_TAGGED: §2.3, §5).  Both give
+ * identical integer results.
+ *
+ * Conventions
+ *  - Every device pointer is a CUDA device address in the current context;
+ *    every buffer is owned by the caller; the library never frees or
+ *    reallocates caller memory and allocates nothing inside rs_pipeline_run.
+ *  - Functions return rs_status; nothing throws across the ABI.  Argument
+ *    and topology errors are reported synchronously before any launch;
+ *    rs_last_error() gives a thread-local detail string.
+ *  - rs_pipeline_run enqueues on `stream` and returns immediately; results
+ *    and statistics are valid once the stream is synchronised.
+ *  - A pipeline handle must not be used by two threads at once.  Distinct
+ *    handles (with distinct workspaces) may run concurrently.
+ */
+#ifndef RS_H
+#define RS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same object as cudaStream_t / CUstream; NULL = the legacy default stream. */
+typedef struct CUstream_st *rs_stream;
+
+typedef enum {
+    RS_OK = 0,
+    RS_ERR_INVALID_ARG = -1,       /* null pointer, bad size, misaligned buffer, ...      */
+    RS_ERR_INVALID_TOPOLOGY = -2,  /* node list is not ENUMERATE (FILTER|TRANSFORM)* AGG  */
+    RS_ERR_UNSUPPORTED = -3,       /* op/dtype combination or config value not built      */
+    RS_ERR_WORKSPACE = -4,         /* workspace missing or smaller than the query         */
+    RS_ERR_CUDA = -5,              /* a CUDA call or launch failed                        */
+    RS_ERR_PROTOCOL = -6           /* device detected a protocol violation (rs_pipeline_check) */
+} rs_status;
+
+/* Node kinds of the linear pipeline (§2.1; DAGs and cycles are
+ * excluded by the paper). */
+typedef enum {
+    RS_NODE_ENUMERATE = 1,   /* parent -> its elements, findCount = offsets  */
+    RS_NODE_FILTER = 2,      /* keep or drop each item (0..1 outputs per input)          */
+    RS_NODE_TRANSFORM = 3,   /* rewrite each item (exactly 1 output per input)           */
+    RS_NODE_AGGREGATE = 4    /* one result per parent (begin/run/end)         */
+} rs_node_kind;
+
+/* Operations.  The paper leaves isGood() and the aggregate open (P:529,
+ * P:532-534); the built-in set is DESIGN.md reading A13/A14/A16/A19. */
+typedef enum {
+    RS_OP_NONE = 0,          /* ENUMERATE                                                  */
+    /* FILTER ops */
+    RS_OP_HASH_LT = 1,       /* keep iff ((uint32)v * p0) >> 24 < p1;  p0 odd, p1 in 0..256 */
+    RS_OP_LT_U32 = 2,        /* keep iff (uint32)v < p1;               p1 in 0..2^32       */
+    RS_OP_CLASS = 3,         /* keep iff bit v of the 32-byte bitmap `table` is set (u8)   */
+    /* TRANSFORM ops */
+    RS_OP_SCALE_F32 = 10,    /* v = p0_as_float * v, fp32 round-to-nearest, no FMA (f32)   */
+    RS_OP_AFFINE_I32 = 11,   /* v = (uint32)(v * p0 + p1)  (i32 / u32)                     */
+    /* AGGREGATE ops (output arrays in rs_aggregates, one entry per region)   */
+    RS_OP_SUM_I64 = 20,      /* elem i32: v0 = int64 sum                                    */
+    RS_OP_SUM_F32 = 21,      /* elem f32: v0 = float sum (fp32 accumulation)               */
+    RS_OP_COUNT_MIN_U32 = 22,/* elem u32: v0 = uint32 count, v1 = uint32 min (0xFFFFFFFF if none) */
+    RS_OP_COUNT_XOR64 = 23   /* elem u8 : v0 = uint64 count, v1 = uint64 xor of mix64(i<<8|byte) */
+} rs_op;
+
+typedef enum { RS_I32 = 0, RS_U32 = 1, RS_U8 = 2, RS_F32 = 3 } rs_dtype;
+
+typedef enum {
+    RS_STRATEGY_SIGNAL = 0,  /* Begin/End signals with credits (§3, §4.2)  */
+    RS_STRATEGY_TAGGED = 1   /* per-item region tags          */
+} rs_strategy;
+
+typedef struct {
+    int32_t kind;            /* rs_node_kind                                         */
+    int32_t op;              /* rs_op                                                */
+    uint64_t p0, p1;         /* op parameters (see rs_op)                            */
+    const uint8_t *table;    /* host pointer, 32 bytes, RS_OP_CLASS only; copied at create */
+} rs_node;
+
+enum {
+    RS_FLAG_STATS = 1u,      /* collect per-node occupancy counters (default on)     */
+    RS_FLAG_VALIDATE = 2u,   /* device-check offsets monotone and <= n_elems          */
+    RS_FLAG_TIMING = 4u      /* record CUDA events around each kernel of a run        */
+};
+
+typedef struct {
+    int32_t strategy;        /* rs_strategy                                          */
+    uint32_t simd_width;     /* ensemble capacity w in items; only 128 is built */
+    uint32_t queue_cap;      /* inter-stage data queue capacity (items, power of 2, >= 2w) */
+    uint32_t signal_cap;     /* signal queue capacity (entries, power of 2, >= 4)    */
+    int32_t grid;            /* persistent CTAs; 0 = fill the device                  */
+    uint32_t chunk;          /* children per parent-stream claim; 0 = default        */
+    uint32_t flags;          /* RS_FLAG_*                                            */
+} rs_config;
+
+/* Per-node occupancy counters (§2.2, §5).  Node 0 is the
+ * enumerate node: items = children enumerated, signal_firings = signals
+ * emitted.  For the other nodes: data_firings = ensembles run,
+ * full_firings = ensembles of exactly w items, items = items consumed,
+ * signal_firings = signals consumed.  Lane fraction = items/(w*data_firings). */
+typedef struct {
+    uint64_t data_firings, full_firings, items, signal_firings;
+} rs_node_stats;
+
+/* Caller-owned per-region outputs (layout per aggregate op above). */
+typedef struct { void *v0; void *v1; } rs_aggregates;
+
+typedef struct rs_pipeline rs_pipeline;
+
+/* Fill `cfg` with defaults (signal strategy, w = 128, stats on). */
+rs_status rs_config_default(rs_config *cfg);
+
+/* Build a pipeline from a node list (BASELINE north star: "create pipeline
+ * from a node list").  The list must be ENUMERATE, then 0..4 FILTER/TRANSFORM
+ * nodes, then one AGGREGATE (single-level enumeration).  `elem` is the
+ * element type of the parents' payload.  Errors: RS_ERR_INVALID_TOPOLOGY,
+ * RS_ERR_UNSUPPORTED (op/dtype mismatch, w != 128, capacities), RS_ERR_INVALID_ARG. */
+rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem,
+                             const rs_config *cfg, rs_pipeline **out);
+
+/* Device workspace needed by rs_pipeline_run for up to `n_regions` regions
+ * over an element array of `n_elems` elements.  Any 256-byte aligned device
+ * buffer of at least this size may be passed; it is overwritten by every run. */
+rs_status rs_pipeline_workspace_bytes(const rs_pipeline *p, int64_t n_regions, int64_t n_elems,
+                                      size_t *bytes);
+
+/* Run the pipeline over regions j = 0..n_regions-1, where region j owns
+ * d_elems[d_offsets[j] .. d_offsets[j+1]) (CSR, int64, non-decreasing, n_regions+1
+ * entries, d_offsets[0] may be > 0 so a batch or shard can address a slice of a
+ * larger stream).  Empty regions are legal.  Writes exactly one
+ * aggregate per region into out.v0[j] (and out.v1[j]) (A2).
+ *   d_elems     device, 16-byte aligned, n_elems elements of the create-time dtype;
+ *               d_offsets[n_regions] <= n_elems is required (checked on device only
+ *               with RS_FLAG_VALIDATE).  May be NULL when n_elems == 0.
+ *   n_regions   0 .. 2^31-1.
+ *   d_ws        workspace of >= rs_pipeline_workspace_bytes(p, n_regions, n_elems).
+ * Asynchronous on `stream`. */
+rs_status rs_pipeline_run(rs_pipeline *p, const void *d_elems, int64_t n_elems,
+                          const int64_t *d_offsets, int64_t n_regions, rs_aggregates out,
+                          void *d_ws, size_t ws_bytes, rs_stream stream);
+
+/* End-to-end convenience: same as rs_pipeline_run but with HOST buffers.
+ * Copies elements and offsets host->device (pinned host memory gives
+ * asynchronous copies), runs, and copies the aggregates back into h_out;
+ * device buffers are owned by the handle and grown on demand.  Synchronises
+ * `stream` before returning. */
+rs_status rs_pipeline_run_host(rs_pipeline *p, const void *h_elems, int64_t n_elems,
+                               const int64_t *h_offsets, int64_t n_regions, rs_aggregates h_out,
+                               rs_stream stream);
+
+/* Copy the per-node counters of the last run into host_out[0..n_nodes-1]
+ * (n_nodes = the create-time node count).  Synchronises `stream`. */
+rs_status rs_pipeline_stats(rs_pipeline *p, rs_node_stats *host_out, int n_nodes, rs_stream stream);
+
+/* Read the device error word of the last run (synchronises `stream`).
+ * Returns RS_ERR_PROTOCOL and sets *code (if non-NULL) when the device saw a
+ * violated invariant: 1 = bad offsets (VALIDATE), 2 = watchdog (no progress),
+ * 3 = signal queue overflow, 4 = unmatched End, 5 = queue overflow. */
+rs_status rs_pipeline_check(rs_pipeline *p, rs_stream stream, int32_t *code);
+
+/* Device time of the last run's kernels (needs RS_FLAG_TIMING; synchronises
+ * `stream`): ms[0] = prepass, ms[1] = persistent pipeline kernel, ms[2] = fixup. */
+rs_status rs_pipeline_kernel_times(rs_pipeline *p, float *ms3, rs_stream stream);
+
+/* Number of kernel launches the last rs_pipeline_run enqueued. */
+int rs_pipeline_launches(const rs_pipeline *p);
+
+/* Persistent CTAs and warps (pipeline instances) per CTA of the last run. */
+rs_status rs_pipeline_geometry(const rs_pipeline *p, int32_t *grid, int32_t *warps_per_cta,
+                               int32_t *chunk);
+
+void rs_pipeline_destroy(rs_pipeline *p);
+
+const char *rs_status_string(rs_status s);
+const char *rs_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RS_H */

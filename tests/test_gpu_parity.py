@@ -1,0 +1,290 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Integer aggregates and counts must match bit-exactly; fp32 sums within a
+relative 1e-5 (north star; DESIGN.md §3 A15).  Inputs are seeded synthetic
+streams with the shapes of BASELINE.json's configs (synth/).
+"""
+import math
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+AGG_DTYPE = {"sum_i64": "i32", "sum_f32": "f32", "count_min_u32": "u32"}
+
+
+@pytest.fixture(scope="module")
+def rs():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2006_07478_b200 as rs
+    return rs
+
+
+def run_gpu(rs, vals, off, stages, agg, strategy="signal", elems_pad=0, **cfg):
+    p = rs.Pipeline(stages, agg, strategy=strategy, **cfg)
+    dev = torch.device("cuda:0")
+    e = torch.from_numpy(np.ascontiguousarray(vals)).to(dev)
+    o = torch.from_numpy(np.ascontiguousarray(off)).to(dev)
+    R = off.size - 1
+    out = p.alloc_outputs(R, dev)
+    ws = p.alloc_workspace(R, e.numel(), dev)
+    p.run(e, o, out, ws)
+    torch.cuda.synchronize()
+    code = p.check()
+    assert code == 0, f"device error {code}"
+    res = [t.cpu().numpy() if t is not None else None for t in out]
+    if agg == "count_min_u32":
+        res = [r.view(np.uint32) for r in res]
+    return res, p.stats(), p
+
+
+def assert_parity(got, ref, agg):
+    if agg == "sum_f32":
+        r = ref[0]
+        g = got[0].astype(np.float64)
+        err = np.abs(g - r)
+        tol = 1e-5 * np.abs(r)
+        bad = np.nonzero(err > tol)[0]
+        assert bad.size == 0, f"{bad.size} fp32 regions out of tolerance, e.g. r={bad[:3]} got={g[bad[:3]]} ref={r[bad[:3]]}"
+    else:
+        for g, r in zip(got, ref):
+            if r is None:
+                continue
+            bad = np.nonzero(g != r)[0]
+            assert bad.size == 0, f"{bad.size} regions differ, first {bad[:5]} got {g[bad[:5]]} ref {r[bad[:5]]}"
+
+
+@pytest.mark.parametrize("strategy", ["signal", "tagged"])
+def test_tiny_d1(rs, strategy):
+    vals, off, stages, agg = synth.tiny()
+    ref = oracle.brute(vals, off, stages, agg)
+    got, st, _ = run_gpu(rs, vals, off, stages, agg, strategy)
+    assert_parity(got, ref, agg)
+    kc = oracle.node_counts(vals, off, stages)
+    assert st[0][2] == off[-1] - off[0]                      # enumerated children = sum of sizes
+    for j in range(len(stages) + 1):
+        assert st[j + 1][2] == kc[:, j].sum()                # items reaching each node
+    if strategy == "signal":
+        assert st[0][3] == 2 * (off.size - 1)                # Begin + End per parent
+        bound = oracle.occupancy_bound(kc, 128)
+        for j in range(len(stages) + 1):
+            lane = st[j + 1][2] / (128 * st[j + 1][0])
+            assert lane <= bound[j] + 1e-12
+
+
+def _case(seed, agg, R=None, dist=None, L=None, base=None):
+    rnd = random.Random(seed)
+    R = R if R is not None else rnd.choice([1, 7, 100, 1000, 5000])
+    dist = dist or rnd.choice(["fixed", "var", "uniform", "zipf"])
+    L = L if L is not None else rnd.choice([0, 1, 3, 17, 128, 129, 700, 5000])
+    lens = synth.lengths(R, dist, L=L, lo=0, hi=max(1, 2 * L), seed=seed, zipf_max=max(2, L))
+    base = base if base is not None else rnd.choice([0, 1, 2, 3, 5])
+    off = synth.offsets(lens, base=base)
+    vals = synth.values(int(off[-1]) + rnd.randint(0, 7), AGG_DTYPE[agg], seed=seed + 1)
+    nst = rnd.randint(0, 4)
+    stages = []
+    for k in range(nst):
+        if agg == "count_min_u32":
+            stages.append(("lt_u32", rnd.choice([0, 1 << 31, 1 << 32, rnd.getrandbits(32)])))
+        elif agg == "sum_f32" and rnd.random() < 0.4:
+            stages.append(("scale_f32", 3.14))
+        elif agg == "sum_i64" and rnd.random() < 0.3:
+            stages.append(("affine_i32", rnd.getrandbits(32), rnd.getrandbits(32)))
+        else:
+            stages.append(("hash_lt", rnd.getrandbits(32) | 1, rnd.choice([0, 64, 192, 256])))
+    return vals, off, stages
+
+
+@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("strategy", ["signal", "tagged"])
+def test_random_parity(rs, seed, strategy):
+    agg = ["sum_i64", "sum_f32", "count_min_u32"][seed % 3]
+    vals, off, stages = _case(seed, agg)
+    rnd = random.Random(seed * 7 + 1)
+    cfg = dict(chunk=rnd.choice([2048, 4096, 8192]), grid=rnd.choice([0, 0, 1, 3]),
+               queue_cap=rnd.choice([256, 512]), signal_cap=rnd.choice([4, 16, 128]))
+    ref = oracle.brute(vals, off, stages, agg)
+    got, st, _ = run_gpu(rs, vals, off, stages, agg, strategy, **cfg)
+    assert_parity(got, ref, agg)
+    assert st[0][2] == off[-1] - off[0]
+
+
+@pytest.mark.parametrize("strategy", ["signal", "tagged"])
+@pytest.mark.parametrize("L", [1, 4, 32, 127, 128, 129, 256, 4096, 100000])
+def test_region_lengths(rs, strategy, L):
+    """Region lengths 1..4096 (north star) plus regions far longer than a chunk."""
+    N = 1 << 18
+    R = max(1, N // L)
+    for dist in ("fixed", "var"):
+        lens = synth.lengths(R, dist, L=L, seed=L)
+        off = synth.offsets(lens, base=3)
+        vals = synth.values(int(off[-1]), "i32", seed=L + 5)
+        stages = synth.sweep_stages(3)
+        ref = oracle.brute(vals, off, stages, "sum_i64")
+        got, st, _ = run_gpu(rs, vals, off, stages, "sum_i64", strategy)
+        assert_parity(got, ref, "sum_i64")
+
+
+@pytest.mark.parametrize("strategy", ["signal", "tagged"])
+def test_empty_and_degenerate(rs, strategy):
+    stages = synth.sweep_stages(2)
+    # all regions empty (N = 0)
+    off = np.zeros(50, np.int64)
+    got, st, _ = run_gpu(rs, np.zeros(4, np.int32), off, stages, "sum_i64", strategy)
+    assert (got[0] == 0).all()
+    # a single element; a single huge region; empty regions at chunk boundaries
+    for lens in ([1], [300000], [0] * 3 + [8192 - 3] + [0] * 5 + [8192] + [0, 0, 1]):
+        off = synth.offsets(np.array(lens, np.int64), base=0)
+        vals = synth.values(int(off[-1]) + 1, "i32", seed=1)
+        ref = oracle.brute(vals, off, stages, "sum_i64")
+        got, _, _ = run_gpu(rs, vals, off, stages, "sum_i64", strategy, chunk=2048)
+        assert_parity(got, ref, "sum_i64")
+    # count/min identity for empty regions: count 0, min 0xFFFFFFFF
+    off = np.array([0, 0, 3, 3], np.int64)
+    vals = np.array([5, 2, 9, 0], np.uint32)
+    got, _, _ = run_gpu(rs, vals, off, [("lt_u32", 1 << 32)], "count_min_u32", strategy)
+    assert list(got[0]) == [0, 3, 0] and list(got[1]) == [0xFFFFFFFF, 2, 0xFFFFFFFF]
+
+
+def test_strategies_bit_identical(rs):
+    """Signal and tagged strategies give bit-identical integer aggregates."""
+    lens = synth.lengths(20000, "zipf", seed=3, zipf_max=4096)
+    off = synth.offsets(lens)
+    vals = synth.values(int(off[-1]), "i32", 4)
+    stages = synth.sweep_stages(3)
+    a, _, _ = run_gpu(rs, vals, off, stages, "sum_i64", "signal")
+    b, _, _ = run_gpu(rs, vals, off, stages, "sum_i64", "tagged")
+    np.testing.assert_array_equal(a[0], b[0])
+
+
+def test_batching_invariance(rs):
+    """Aggregates do not depend on batching: sub-ranges of the parent stream
+    with offsets[0] != 0 over the same element array reproduce the full run."""
+    lens = synth.lengths(30000, "var", L=60, seed=8)
+    off = synth.offsets(lens)
+    vals = synth.values(int(off[-1]), "i32", 9)
+    stages = synth.sweep_stages(3)
+    full, _, _ = run_gpu(rs, vals, off, stages, "sum_i64")
+    parts = []
+    for a, b in ((0, 1), (1, 9999), (9999, 10000), (10000, 30000)):
+        g, _, _ = run_gpu(rs, vals, off[a:b + 1], stages, "sum_i64")
+        parts.append(g[0])
+    np.testing.assert_array_equal(np.concatenate(parts), full[0])
+
+
+def test_grid_and_capacity_invariance(rs):
+    lens = synth.lengths(5000, "var", L=40, seed=11)
+    off = synth.offsets(lens)
+    vals = synth.values(int(off[-1]), "i32", 12)
+    stages = synth.sweep_stages(3)
+    ref = oracle.brute(vals, off, stages, "sum_i64")
+    for cfg in (dict(grid=1), dict(grid=2, chunk=2048), dict(queue_cap=1024, signal_cap=8), dict(signal_cap=4)):
+        for strat in ("signal", "tagged"):
+            got, _, _ = run_gpu(rs, vals, off, stages, "sum_i64", strat, **cfg)
+            assert_parity(got, ref, "sum_i64")
+
+
+@pytest.mark.parametrize("R", [32, 64, 96, 128, 256, 512, 1024])
+def test_occupancy_closed_form_gpu(rs, R):
+    """One instance (grid=1), fixed regions dividing the chunk, pass-all
+    stages, full-first: the aggregate's lane fraction equals R/(w ceil(R/w))
+    exactly, as the oracle's interpreter gives."""
+    nreg = (1 << 16) // R
+    off = np.arange(0, nreg * R + 1, R, dtype=np.int64)
+    vals = synth.values(int(off[-1]), "i32", R)
+    stages = [("hash_lt", 0x9E3779B1, 256)] * 2
+    got, st, _ = run_gpu(rs, vals, off, stages, "sum_i64", "signal", grid=1, chunk=8192)
+    ref = oracle.interp(vals, off, stages, "sum_i64", w=128, qcap=1024, scap=256)
+    np.testing.assert_array_equal(got[0], ref["out"][0])
+    num, den = R, 128 * math.ceil(R / 128)
+    for n in range(1, len(stages) + 2):
+        assert st[n][2] * den == st[n][0] * 128 * num, (n, st[n])
+        assert st[n][0] == ref["stats"][n][0]
+
+
+def test_tagged_full_ensembles(rs):
+    """Tagged strategy keeps ensembles full regardless of region length."""
+    lens = synth.lengths(1 << 16, "fixed", L=3)
+    off = synth.offsets(lens)
+    vals = synth.values(int(off[-1]), "i32", 2)
+    got, st, _ = run_gpu(rs, vals, off, [("hash_lt", 3, 256)], "sum_i64", "tagged", grid=1)
+    assert st[1][1] >= st[1][0] - 2       # all but the stream-tail ensembles are full
+
+
+def test_validate_flag_catches_bad_offsets(rs):
+    vals = synth.values(100, "i32", 0)
+    off = np.array([0, 50, 40, 100], np.int64)
+    p = rs.Pipeline([], "sum_i64", flags=rs.RS_FLAG_STATS | rs.RS_FLAG_VALIDATE)
+    e = torch.from_numpy(vals).cuda()
+    o = torch.from_numpy(off).cuda()
+    out = p.alloc_outputs(3)
+    ws = p.alloc_workspace(3, 100)
+    p.run(e, o, out, ws)
+    torch.cuda.synchronize()
+    with pytest.raises(rs.RSError):
+        p.check()
+    # offsets beyond n_elems are caught even without VALIDATE (no out-of-bounds TMA)
+    p2 = rs.Pipeline([], "sum_i64")
+    o2 = torch.tensor([0, 50, 200], dtype=torch.int64, device="cuda")
+    out2 = p2.alloc_outputs(2)
+    ws2 = p2.alloc_workspace(2, 100)
+    p2.run(e, o2, out2, ws2)
+    torch.cuda.synchronize()
+    with pytest.raises(rs.RSError):
+        p2.check()
+
+
+def test_run_host_e2e(rs):
+    vals, off, stages, agg = synth.tiny()
+    ref = oracle.brute(vals, off, stages, agg)[0]
+    p = rs.Pipeline(stages, agg)
+    out = np.zeros(off.size - 1, np.int64)
+    p.run_host(vals, off, out)
+    np.testing.assert_array_equal(out, ref)
+
+
+@pytest.mark.parametrize("strategy", ["signal", "tagged"])
+def test_full_size_sampled(rs, strategy):
+    """BASELINE config sizes in the bench launch configuration: N = 2^29 int32
+    children, L = 4096 (and Zipf), 3 filters; oracle on sampled regions plus
+    the device-side child-count invariant."""
+    N = 1 << 29
+    for dist, L in (("fixed", 4096), ("zipf", 0)):
+        if dist == "fixed":
+            lens = torch.full((N // L,), L, dtype=torch.int64, device="cuda")
+        else:
+            lens = synth.torch_lengths(N // 208, "zipf", seed=5, device="cuda")
+        off = synth.torch_offsets(lens)
+        n = int(off[-1].item())
+        vals = synth.torch_values(n, "i32", seed=7, device="cuda")
+        stages = synth.sweep_stages(3)
+        p = rs.Pipeline(stages, "sum_i64", strategy=strategy)
+        R = off.numel() - 1
+        out = p.alloc_outputs(R)
+        ws = p.alloc_workspace(R, n)
+        p.run(vals, off, out, ws)
+        torch.cuda.synchronize()
+        assert p.check() == 0
+        st = p.stats()
+        assert st[0][2] == n
+        rng = np.random.default_rng(1)
+        idx = np.unique(np.concatenate([rng.integers(0, R, 400), [0, R - 1]]))
+        off_h = off.cpu().numpy()
+        got = out[0].cpu().numpy()
+        for r in idx:
+            a, b = int(off_h[r]), int(off_h[r + 1])
+            v = vals[a:b].cpu().numpy()
+            ref = oracle.brute(v, np.array([0, b - a], np.int64), stages, "sum_i64")[0][0]
+            assert got[r] == ref, (dist, r)
+        del vals, off, out, ws
+        torch.cuda.empty_cache()
