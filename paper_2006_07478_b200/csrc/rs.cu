@@ -570,9 +570,10 @@ struct Pipe {
             const uint32_t a = admissible(ei, spend);
             uint32_t ar = a;
             if (ei == 0) {
-                uint32_t rdy = ready_lim - qh[0];
-                if ((int)rdy < 0) rdy = 0;
-                if (rdy < ar) { ready_lim = landed_pos(); rdy = ready_lim - qh[0]; ar = min(ar, rdy); }
+                // only items whose TMA stage has landed may be read
+                if ((int)(ready_lim - qh[0]) < (int)ar) ready_lim = landed_pos();
+                const int rdy = (int)(ready_lim - qh[0]);
+                ar = rdy <= 0 ? 0u : min(ar, (uint32_t)rdy);
             }
             uint32_t space = 0xffffffffu;
             if constexpr (!AGGN) space = qcap - (qt[n] - qh[n]);
@@ -708,8 +709,9 @@ struct Pipe {
             if (lane == 0 && head && akey != 0xffffffffu) store_key(akey, carry);
             const bool nexthead = (lane < 31) && ((hm >> (lane + 1)) & 1u);
             if (act && nexthead) store_key(key, v);      // complete segment inside the slice
-            akey = __shfl_sync(kFull, key, cntj - 1);
-            carry = AT::shfl(v, cntj - 1);
+            const int last = (cntj < 32 ? cntj : 32) - 1;   // last active lane of this slice
+            akey = __shfl_sync(kFull, key, last);
+            carry = AT::shfl(v, last);
         }
     }
 

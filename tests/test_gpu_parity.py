@@ -75,7 +75,12 @@ def test_tiny_d1(rs, strategy):
     for j in range(len(stages) + 1):
         assert st[j + 1][2] == kc[:, j].sum()                # items reaching each node
     if strategy == "signal":
-        assert st[0][3] == 2 * (off.size - 1)                # Begin + End per parent
+        # Begin + End per region part: regions crossing a chunk boundary are
+        # split into one part per chunk they touch (A18)
+        C = rs.Pipeline(stages, agg).geometry()["chunk"] or 8192
+        b = np.arange(C, int(off[-1]), C)
+        splits = sum(int(((off[:-1] < x) & (off[1:] > x)).sum()) for x in b)
+        assert st[0][3] == 2 * (off.size - 1 + splits)
         bound = oracle.occupancy_bound(kc, 128)
         for j in range(len(stages) + 1):
             lane = st[j + 1][2] / (128 * st[j + 1][0])
@@ -203,7 +208,8 @@ def test_occupancy_closed_form_gpu(rs, R):
     off = np.arange(0, nreg * R + 1, R, dtype=np.int64)
     vals = synth.values(int(off[-1]), "i32", R)
     stages = [("hash_lt", 0x9E3779B1, 256)] * 2
-    got, st, _ = run_gpu(rs, vals, off, stages, "sum_i64", "signal", grid=1, chunk=8192)
+    chunk = 1 << max(11, int(off[-1] - 1).bit_length())     # one chunk: no region is split
+    got, st, _ = run_gpu(rs, vals, off, stages, "sum_i64", "signal", grid=1, chunk=chunk)
     ref = oracle.interp(vals, off, stages, "sum_i64", w=128, qcap=1024, scap=256)
     np.testing.assert_array_equal(got[0], ref["out"][0])
     num, den = R, 128 * math.ceil(R / 128)
