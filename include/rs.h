@@ -102,7 +102,7 @@ enum {
 typedef struct {
     int32_t strategy;        /* rs_strategy                                          */
     uint32_t simd_width;     /* ensemble capacity w in items; only 128 is built */
-    uint32_t queue_cap;      /* inter-stage data queue capacity (items, power of 2, >= 2w) */
+    uint32_t queue_cap;      /* inter-stage data queue capacity (items, power of 2, >= 2w; default 8w) */
     uint32_t signal_cap;     /* signal queue capacity (entries, power of 2, >= 4)    */
     int32_t grid;            /* persistent CTAs; 0 = fill the device                  */
     uint32_t chunk;          /* children per parent-stream claim; 0 = default        */

@@ -177,627 +177,7 @@ __global__ void k_fixup(KParams P) {
 }
 
 // ---------------------------------------------------------- the pipeline
-template <int K, int AGG, bool TAG>
-struct Pipe {
-    using AT = AggT<AGG>;
-    using A = typename AT::A;
-    static constexpr int SBLK = TAG ? 256 : 512;     // elements per TMA stage
-    static constexpr int RING0 = NST * SBLK;         // Q0 ring capacity (items)
-
-    const KParams &P;
-    const int lane;
-    // shared-memory rings
-    uint64_t *bar;                 // [NST]
-    uint32_t *q[K + 1];            // data rings: q[0] = Q0 (RING0), q[e] = Q_e (qcap)
-    uint32_t *t[K + 1];            // tag rings (tagged strategy)
-    uint2 *s[K + 1];               // signal rings {key, credit | END_BIT}
-    uint32_t qmask, smask, qcap, scap;
-
-    // edge e : node e -> node e+1
-    uint32_t qh[K + 1], qt[K + 1];     // data queue head/tail (monotone positions)
-    uint32_t sh[K + 1], stl[K + 1];    // signal queue head/tail
-    uint32_t sent[K + 1];              // sender: items emitted since last signal
-    uint32_t cur[K + 1];               // receiver current credit counter
-    bool xfer[K + 1];                  // head signal's credit already moved into cur
-    // per-node stats: ensembles, full ensembles, items, signals
-    uint32_t nd[K + 2], nf[K + 2], ni[K + 2], ns[K + 2];
-
-    // chunk FIFO (F0 = being enumerated, F1 = staged next)
-    int32_t fk[2];
-    long long fbeg[2], fend[2];
-    uint32_t fpos[2], ffr0[2], ffr1[2];
-    bool fhead[2];
-    bool claims_done;
-    uint32_t stg_j, landed_j;
-    // enumerate cursor within F0
-    uint32_t pidx;
-    bool begun;
-    bool enum_done;
-    // aggregate state
-    A acc;             // per-lane partial accumulator (signal: current region; tagged: carry key)
-    uint32_t akey;     // signal: open region key; tagged: carry key (0xffffffff = none)
-    A carry;           // tagged: uniform carried partial
-    long long base0, offR;
-    uint32_t nchunks;
-
-    __device__ Pipe(const KParams &p, uint8_t *smem, int lane_) : P(p), lane(lane_) {
-        qcap = P.qcap;
-        scap = P.scap;
-        qmask = qcap - 1;
-        smask = scap - 1;
-        uint8_t *ptr = smem;
-        bar = reinterpret_cast<uint64_t *>(ptr);
-        ptr += 128;
-        q[0] = reinterpret_cast<uint32_t *>(ptr);
-        ptr += RING0 * 4;
-        if (TAG) { t[0] = reinterpret_cast<uint32_t *>(ptr); ptr += RING0 * 4; } else t[0] = nullptr;
-#pragma unroll
-        for (int e = 1; e <= K; ++e) {
-            q[e] = reinterpret_cast<uint32_t *>(ptr);
-            ptr += qcap * 4;
-            if (TAG) { t[e] = reinterpret_cast<uint32_t *>(ptr); ptr += qcap * 4; } else t[e] = nullptr;
-        }
-#pragma unroll
-        for (int e = 0; e <= K; ++e) {
-            s[e] = reinterpret_cast<uint2 *>(ptr);
-            if (!TAG) ptr += scap * 8;
-        }
-#pragma unroll
-        for (int e = 0; e <= K; ++e) { qh[e] = qt[e] = sh[e] = stl[e] = sent[e] = cur[e] = 0; xfer[e] = false; }
-#pragma unroll
-        for (int n = 0; n < K + 2; ++n) nd[n] = nf[n] = ni[n] = ns[n] = 0;
-        fk[0] = fk[1] = -1;
-        claims_done = false;
-        stg_j = landed_j = 0;
-        pidx = 0;
-        begun = false;
-        enum_done = false;
-        acc = AT::id();
-        carry = AT::id();
-        akey = 0xffffffffu;
-        base0 = P.hdr->base0;
-        offR = P.hdr->offR;
-        nchunks = P.hdr->nchunks;
-    }
-
-    __host__ __device__ static constexpr uint32_t smem_bytes(uint32_t qcap, uint32_t scap) {
-        return 128 + RING0 * 4 * (TAG ? 2 : 1) + K * qcap * 4 * (TAG ? 2 : 1) + (TAG ? 0 : (K + 1) * scap * 8);
-    }
-
-    __device__ __forceinline__ uint32_t bcast(uint32_t v) const { return __shfl_sync(kFull, v, 0); }
-
-    // ---------------------------------------------------------- chunks
-    __device__ void load_chunk(int f, int32_t k, uint32_t pos) {
-        fk[f] = k;
-        long long b = (k == 0) ? P.hdr->off0 : base0 + (long long)k * P.C;
-        long long e = base0 + (long long)(k + 1) * P.C;
-        if (e > offR) e = offR;
-        fbeg[f] = b;
-        fend[f] = e;
-        fpos[f] = pos;
-        ffr0[f] = P.chunk_fr[k];
-        ffr1[f] = P.chunk_fr[k + 1];
-        fhead[f] = (k > 0) && (P.off[ffr0[f]] > b);
-    }
-    __device__ __forceinline__ uint32_t flen(int f) const { return (uint32_t)(fend[f] - fbeg[f]); }
-    __device__ __forceinline__ uint32_t nparts0() const { return (fhead[0] ? 1u : 0u) + (ffr1[0] - ffr0[0]); }
-
-    // Claim the next chunk of the parent stream (atomics, no locks).
-    __device__ int32_t claim() {
-        uint32_t k = 0;
-        if (lane == 0) k = atomicAdd(&P.hdr->claim, 1u);
-        k = bcast(k);
-        return k < nchunks ? (int32_t)k : -1;
-    }
-
-    // Issue TMA stage j from FIFO entry f.
-    __device__ void issue_stage(int f) {
-        const uint32_t j = stg_j;
-        const uint32_t p0 = j * SBLK;
-        const uint32_t pend = fpos[f] + flen(f);
-        const uint32_t n = min((uint32_t)SBLK, pend - p0);
-        const long long src = fbeg[f] + (long long)p0 - (long long)fpos[f];   // 4-element aligned
-        uint32_t *dst = q[0] + (p0 & (RING0 - 1));
-        uint64_t *b = &bar[j % NST];
-        const long long lim = (P.n_elems - src) & ~3ll;     // whole 16-byte blocks inside the array
-        const uint32_t ntma = (uint32_t)min((long long)((n + 3u) & ~3u), lim);
-        // tail elements that a 16-byte copy cannot reach without overrunning n_elems
-        const int tail = (int)n - (int)ntma;
-        if (tail > 0 && lane < tail) {
-            const uint32_t *g = reinterpret_cast<const uint32_t *>(P.elems) + src + ntma + lane;
-            dst[ntma + lane] = __ldg(g);
-        }
-        __syncwarp();
-        if (lane == 0) {
-            fence_proxy_async();
-            if (ntma) {
-                mbar_arrive_expect_tx(b, ntma * 4u);
-                tma_load_1d(dst, P.elems + src * 4, ntma * 4u, b);
-            } else {
-                mbar_arrive(b);
-            }
-        }
-        stg_j = j + 1;
-    }
-
-    // Keep the Q0 ring full: prefetch element blocks ahead of the enumerate node.
-    __device__ void refill() {
-        for (;;) {
-            if ((stg_j + 1) * (uint32_t)SBLK > qh[0] + RING0) return;   // ring slot still in use
-            const uint32_t sp = stg_j * SBLK;
-            int f = -1;
-            if (fk[0] >= 0 && sp < fpos[0] + flen(0)) f = 0;
-            else if (fk[1] >= 0 && sp < fpos[1] + flen(1)) f = 1;
-            if (f < 0) {
-                if (fk[1] >= 0 || claims_done) return;
-                int32_t k = claim();
-                if (k < 0) { claims_done = true; return; }
-                if (fk[0] < 0) {
-                    uint32_t pos = (k == 0) ? (uint32_t)(P.hdr->off0 - base0) : sp;
-                    if (k == 0 && stg_j == 0) { qh[0] = qt[0] = pos; }
-                    load_chunk(0, k, pos);
-                    pidx = 0;
-                    begun = false;
-                } else {
-                    load_chunk(1, k, fpos[0] + flen(0));
-                }
-                continue;
-            }
-            issue_stage(f);
-        }
-    }
-
-    // ------------------------------------------------------ enumerate
-    // Part q of chunk F0: [start, end) elements and its key (region id, or a
-    // partial slot for the chunk's head part / a tail part crossing the chunk end).
-    __device__ void part_info(uint32_t qi, bool valid, long long &ps, long long &pe, uint32_t &key) const {
-        ps = pe = fend[0];
-        key = 0;
-        if (!valid) return;
-        if (fhead[0] && qi == 0) {
-            ps = fbeg[0];
-            long long e = P.off[ffr0[0]];
-            pe = e < fend[0] ? e : fend[0];
-            key = SLOT | (uint32_t)(2 * fk[0]);
-        } else {
-            uint32_t r = ffr0[0] + qi - (fhead[0] ? 1u : 0u);
-            ps = P.off[r];
-            long long e = P.off[r + 1];
-            if (e > fend[0]) { pe = fend[0]; key = SLOT | (uint32_t)(2 * fk[0] + 1); }
-            else { pe = e; key = r; }
-        }
-    }
-
-    // Sender rule for one signal on edge e given the queue state at emission
-    // (P:304-312): S empty -> |Q|; otherwise items emitted since the tail signal.
-    __device__ __forceinline__ void push_signal(int e, uint32_t key, bool end, uint32_t credit_rule2) {
-        uint32_t credit = (sh[e] == stl[e]) ? (qt[e] - qh[e]) : credit_rule2;
-        if (lane == 0) s[e][stl[e] & smask] = make_uint2(key, credit | (end ? END_BIT : 0u));
-        stl[e] += 1;
-        sent[e] = 0;
-    }
-
-    // One enumerate firing: emit element indices (as staged element values)
-    // and Begin/End signals of F0's parts as far as staged data and signal
-    // space allow (resumable mid-region).
-    __device__ bool enumerate() {
-        bool prog = false;
-        refill();
-        for (;;) {
-            if (fk[0] < 0) {
-                if (fk[1] >= 0) { shift(); continue; }
-                if (claims_done) enum_done = true;
-                return prog;
-            }
-            const uint32_t np = nparts0();
-            if (pidx >= np) {
-                // chunk fully enumerated; its items are all emitted
-                shift();
-                refill();
-                prog = true;
-                continue;
-            }
-            const uint32_t lim_pos = min(stg_j * (uint32_t)SBLK, fpos[0] + flen(0));
-            const uint32_t avail = lim_pos - qt[0];
-            const long long e_next = fbeg[0] + (long long)(qt[0] - fpos[0]);
-            // batch of up to 32 parts, one per lane
-            const uint32_t qi = pidx + lane;
-            long long ps, pe;
-            uint32_t key;
-            part_info(qi, qi < np, ps, pe, key);
-            if (lane == 0 && ps < e_next) ps = e_next;     // resume inside part pidx
-            uint32_t cnt = (uint32_t)(pe - ps);
-            // inclusive scan of counts (and signals) across the batch
-            uint32_t cum = cnt;
-            uint32_t sig = TAG ? 0u : ((lane == 0 && begun) ? 1u : 2u);
-            uint32_t scum = sig;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                uint32_t o = __shfl_up_sync(kFull, cum, d);
-                uint32_t so = __shfl_up_sync(kFull, scum, d);
-                if (lane >= d) { cum += o; scum += so; }
-            }
-            const uint32_t sfree = TAG ? 0xffffffffu : scap - (stl[0] - sh[0]);
-            const bool fits = (qi < np) && (cum <= avail) && (scum <= sfree);
-            const uint32_t m = __popc(__ballot_sync(kFull, fits));
-            if (m > 0) {
-                const uint32_t tot = __shfl_sync(kFull, cum, m - 1);
-                if constexpr (!TAG) {
-                    // Signals of parts 0..m-1: Begin_i, End_i in stream order.
-                    const bool empty_at_start = (sh[0] == stl[0]);
-                    const uint32_t qlen0 = qt[0] - qh[0];
-                    const uint32_t sexcl = scum - sig;
-                    if (lane < (int)m) {
-                        uint32_t slot = stl[0] + sexcl;
-                        if (!(lane == 0 && begun)) {
-                            // Begin_i: first signal of the batch uses rule (1) if S was empty,
-                            // else rule (2) with items since the previous signal (sent[0]);
-                            // later Begins follow an End directly: credit 0.
-                            uint32_t c = (lane == 0) ? (empty_at_start ? qlen0 : sent[0]) : 0u;
-                            s[0][slot & smask] = make_uint2(key, c);
-                            slot++;
-                        }
-                        // End_i: items of part i since its Begin (rule 2), or rule (1) when
-                        // part 0 began earlier and S has since been drained by the receiver.
-                        uint32_t c;
-                        if (lane == 0 && begun) c = empty_at_start ? (qlen0 + cnt) : (sent[0] + cnt);
-                        else c = cnt;
-                        s[0][slot & smask] = make_uint2(key, c | END_BIT);
-                    }
-                    stl[0] += __shfl_sync(kFull, scum, m - 1);
-                    ns[0] += __shfl_sync(kFull, scum, m - 1);
-                    sent[0] = 0;
-                } else {
-                    write_tags(m, cum, cnt, key, tot);
-                }
-                qt[0] += tot;
-                ni[0] += tot;
-                pidx += m;
-                begun = false;
-                prog = true;
-                __syncwarp();
-                continue;
-            }
-            // Part pidx does not fit whole: emit what we can of it (resumable).
-            const uint32_t key0 = __shfl_sync(kFull, key, 0);
-            const uint32_t cnt0 = __shfl_sync(kFull, cnt, 0);
-            bool did = false;
-            if constexpr (!TAG) {
-                if (!begun) {
-                    if (scap - (stl[0] - sh[0]) == 0) return prog;
-                    push_signal(0, key0, false, sent[0]);
-                    ns[0]++;
-                    begun = true;
-                    did = true;
-                }
-            }
-            const uint32_t k = min(avail, cnt0);
-            if (k > 0) {
-                if constexpr (TAG) write_tags_uniform(key0, k);
-                qt[0] += k;
-                sent[0] += k;
-                ni[0] += k;
-                did = true;
-            }
-            if constexpr (!TAG) {
-                if (k == cnt0 && scap - (stl[0] - sh[0]) > 0) {
-                    push_signal(0, key0, true, sent[0]);
-                    ns[0]++;
-                    pidx++;
-                    begun = false;
-                    did = true;
-                }
-            } else {
-                if (k == cnt0) { pidx++; did = true; }
-            }
-            __syncwarp();
-            prog |= did;
-            if (!did) return prog;
-        }
-    }
-
-    __device__ void shift() {
-        fk[0] = fk[1];
-        fbeg[0] = fbeg[1];
-        fend[0] = fend[1];
-        fpos[0] = fpos[1];
-        ffr0[0] = ffr0[1];
-        ffr1[0] = ffr1[1];
-        fhead[0] = fhead[1];
-        fk[1] = -1;
-        pidx = 0;
-        begun = false;
-    }
-
-    // Tagged enumerate: every emitted item gets its parent's key
-    // (P:258-261).  Positions qt[0] .. qt[0]+tot-1 belong to parts
-    // 0..m-1 of this batch (lane i holds part i's inclusive end `cum`).
-    __device__ void write_tags(uint32_t m, uint32_t cum, uint32_t cnt, uint32_t key, uint32_t tot) {
-        if (m == 1 || __shfl_sync(kFull, cnt, 0) == tot) {
-            write_tags_uniform(__shfl_sync(kFull, key, 0), tot);
-            return;
-        }
-        const uint32_t excl = cum - cnt;
-        for (uint32_t base = 0; base < tot; base += 32) {
-            const uint32_t rel = base + lane;
-            // largest part i < m with excl_i <= rel (binary search over lanes)
-            int lo = 0;
-#pragma unroll
-            for (int step = 16; step >= 1; step >>= 1) {
-                int cand = lo + step;
-                uint32_t ex = __shfl_sync(kFull, excl, cand < 32 ? cand : 31);
-                if (cand < (int)m && ex <= rel) lo = cand;
-            }
-            const uint32_t k = __shfl_sync(kFull, key, lo);
-            if (rel < tot) t[0][(qt[0] + rel) & (RING0 - 1)] = k;
-        }
-    }
-    __device__ void write_tags_uniform(uint32_t key, uint32_t k) {
-        for (uint32_t i = lane; i < k; i += 32) t[0][(qt[0] + i) & (RING0 - 1)] = key;
-    }
-
-    // ---------------------------------------------------------- stages
-    __device__ __forceinline__ uint32_t landed_pos() {
-        while (landed_j < stg_j && mbar_test(&bar[landed_j % NST], (landed_j / NST) & 1u)) landed_j++;
-        return landed_j * (uint32_t)SBLK;
-    }
-
-    // Receiver admissible count on edge e, applying rule (2b).
-    __device__ __forceinline__ uint32_t admissible(int e, bool &spend) {
-        spend = sh[e] != stl[e];
-        const uint32_t ql = qt[e] - qh[e];
-        if (!spend) return ql;
-        if (cur[e] == 0 && !xfer[e]) {
-            uint32_t c = s[e][sh[e] & smask].y & ~END_BIT;
-            if (c > 0) { cur[e] = c; xfer[e] = true; }
-        }
-        return min(ql, cur[e]);
-    }
-
-    // Fire node n (1..K+1) repeatedly while it can make progress.
-    template <int n>
-    __device__ bool fire(bool drained) {
-        constexpr int ei = n - 1;          // input edge
-        constexpr bool AGGN = (n == K + 1);
-        const uint32_t imask = (ei == 0) ? (RING0 - 1) : qmask;
-        uint32_t *in = q[ei];
-        uint32_t *tin = t[ei];
-        bool prog = false;
-        uint32_t ready_lim = 0;
-        if (ei == 0) ready_lim = landed_pos();
-        for (;;) {
-            bool spend;
-            const uint32_t a = admissible(ei, spend);
-            uint32_t ar = a;
-            if (ei == 0) {
-                // only items whose TMA stage has landed may be read
-                if ((int)(ready_lim - qh[0]) < (int)ar) ready_lim = landed_pos();
-                const int rdy = (int)(ready_lim - qh[0]);
-                ar = rdy <= 0 ? 0u : min(ar, (uint32_t)rdy);
-            }
-            uint32_t space = 0xffffffffu;
-            if constexpr (!AGGN) space = qcap - (qt[n] - qh[n]);
-            uint32_t e = min(min(ar, (uint32_t)W), space);
-            bool ok = e > 0;
-            if (ok && e < (uint32_t)W) {
-                const bool bounded = spend && e == cur[ei];
-                const bool dr = drained && e == a;
-                ok = bounded || dr;
-            }
-            if (ok) {
-                run_ensemble<n>(in, tin, imask, qh[ei], e);
-                qh[ei] += e;
-                if (spend) cur[ei] -= e;
-                nd[n]++;
-                ni[n] += e;
-                if (e == (uint32_t)W) nf[n]++;
-                prog = true;
-                continue;
-            }
-            // signal phase: only with the counter at 0
-            if constexpr (TAG) break;
-            if (!spend || cur[ei] != 0) break;
-            const uint2 hs = s[ei][sh[ei] & smask];
-            if (!xfer[ei] && (hs.y & ~END_BIT) > 0) {
-                cur[ei] = hs.y & ~END_BIT;
-                xfer[ei] = true;
-                continue;
-            }
-            if constexpr (!AGGN) {
-                if (scap - (stl[n] - sh[n]) == 0) break;
-            }
-            sh[ei]++;
-            xfer[ei] = false;
-            ns[n]++;
-            prog = true;
-            const bool is_end = (hs.y & END_BIT) != 0;
-            if constexpr (AGGN) {
-                if (!is_end) {               // a::begin: acc = identity
-                    acc = AT::id();
-                    akey = hs.x;
-                } else {                     // a::end: push(acc)
-                    A v = warp_reduce<AT>(acc);
-                    if (lane == 0) store_key(hs.x, v);
-                    acc = AT::id();
-                    akey = 0xffffffffu;
-                }
-            } else {
-                push_signal(n, hs.x, is_end, sent[n]);   // forwarded with a fresh credit
-            }
-        }
-        __syncwarp();
-        return prog;
-    }
-
-    __device__ __forceinline__ void store_key(uint32_t key, A v) {
-        if (key & SLOT) AT::store(P.part0, P.part1, key & ~SLOT, v);
-        else AT::store(P.out0, P.out1, key, v);
-    }
-
-    template <int n>
-    __device__ __forceinline__ void run_ensemble(const uint32_t *in, const uint32_t *tin, uint32_t imask,
-                                                 uint32_t h, uint32_t e) {
-        if constexpr (n == K + 1) {
-            if constexpr (!TAG) {
-#pragma unroll
-                for (int j = 0; j < IPL; ++j) {
-                    const uint32_t idx = j * 32 + lane;
-                    if (idx < e) acc = AT::comb(acc, AT::lift(in[(h + idx) & imask]));
-                }
-            } else {
-                agg_tagged(in, tin, imask, h, e);
-            }
-        } else {
-            const StageP &sp = P.st[n - 1];
-            uint32_t *out = q[n];
-            uint32_t *tout = t[n];
-            uint32_t tl = qt[n];
-#pragma unroll
-            for (int j = 0; j < IPL; ++j) {
-                const uint32_t idx = j * 32 + lane;
-                const bool act = idx < e;
-                uint32_t v = act ? in[(h + idx) & imask] : 0u;
-                uint32_t tg = 0;
-                if constexpr (TAG) tg = act ? tin[(h + idx) & imask] : 0u;
-                const bool keep = act && stage_apply(sp, v);
-                const uint32_t mk = __ballot_sync(kFull, keep);   // stable compaction
-                if (keep) {
-                    const uint32_t pos = (tl + __popc(mk & lanemask_lt())) & qmask;
-                    out[pos] = v;
-                    if constexpr (TAG) tout[pos] = tg;
-                }
-                tl += __popc(mk);
-            }
-            sent[n] += tl - qt[n];
-            qt[n] = tl;
-            __syncwarp();
-        }
-    }
-
-    // Region-id-keyed segmented reduction with a carry across ensembles
-    // (tagged aggregate).  Ensembles may mix regions.
-    __device__ void agg_tagged(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h, uint32_t e) {
-#pragma unroll
-        for (int j = 0; j < IPL; ++j) {
-            const int cntj = (int)e - j * 32;
-            if (cntj <= 0) break;
-            const bool act = lane < cntj;
-            const uint32_t idx = j * 32 + lane;
-            const uint32_t key = act ? tin[(h + idx) & imask] : 0xffffffffu;
-            const A val = act ? AT::lift(in[(h + idx) & imask]) : AT::id();
-            if (__all_sync(kFull, !act || key == akey)) {
-                acc = AT::comb(acc, val);      // fast path: whole slice continues the carry region
-                continue;
-            }
-            // fold per-lane partials of the carry into `carry`
-            carry = AT::comb(carry, warp_reduce<AT>(acc));
-            acc = AT::id();
-            uint32_t prev = __shfl_up_sync(kFull, key, 1);
-            if (lane == 0) prev = akey;
-            const bool head = act && key != prev;
-            const uint32_t hm = __ballot_sync(kFull, head);
-            const uint32_t le = hm & lanemask_le();
-            const int seg = le ? 31 - __clz(le) : -1;     // first lane of my segment (-1: carry segment)
-            A v = val;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const A o = AT::shfl_up(v, d);
-                if (lane - d >= seg && lane >= d) v = AT::comb(o, v);
-            }
-            if (seg < 0 && act) v = AT::comb(carry, v);
-            // the carry region ended exactly before this slice
-            if (lane == 0 && head && akey != 0xffffffffu) store_key(akey, carry);
-            const bool nexthead = (lane < 31) && ((hm >> (lane + 1)) & 1u);
-            if (act && nexthead) store_key(key, v);      // complete segment inside the slice
-            const int last = (cntj < 32 ? cntj : 32) - 1;   // last active lane of this slice
-            akey = __shfl_sync(kFull, key, last);
-            carry = AT::shfl(v, last);
-        }
-    }
-
-    __device__ void flush_tagged() {
-        carry = AT::comb(carry, warp_reduce<AT>(acc));
-        acc = AT::id();
-        if (lane == 0 && akey != 0xffffffffu) store_key(akey, carry);
-        akey = 0xffffffffu;
-        carry = AT::id();
-    }
-
-    __device__ bool all_empty() const {
-        bool e = true;
-#pragma unroll
-        for (int k = 0; k <= K; ++k) e = e && (qh[k] == qt[k]) && (sh[k] == stl[k]);
-        return e;
-    }
-
-    template <int n>
-    __device__ bool fire_chain(bool drained) {
-        if constexpr (n > K + 1) {
-            return false;
-        } else {
-            bool p = fire<n>(drained);
-            const bool dn = drained && (qh[n - 1] == qt[n - 1]) && (sh[n - 1] == stl[n - 1]);
-            return fire_chain<n + 1>(dn) | p;
-        }
-    }
-
-    __device__ void run() {
-        if (lane == 0)
-            for (int i = 0; i < NST; ++i) mbar_init(&bar[i], 1);
-        mbar_fence_init();
-        __syncwarp();
-        uint32_t idle = 0;
-        for (;;) {
-            bool prog = enumerate();
-            prog |= fire_chain<1>(enum_done);
-            if (enum_done && all_empty()) break;
-            if (prog) { idle = 0; continue; }
-            // nothing fireable: wait for the oldest in-flight TMA stage
-            if (landed_j < stg_j) {
-                uint32_t spins = 0;
-                while (!mbar_try_wait(&bar[landed_j % NST], (landed_j / NST) & 1u)) {
-                    if (++spins > (1u << 24)) break;
-                }
-                if (spins > (1u << 24)) { if (lane == 0) atomicCAS((int *)&P.hdr->err, 0, ERR_WATCHDOG); break; }
-                continue;
-            }
-            if (++idle > 64) {
-                if (lane == 0) atomicCAS((int *)&P.hdr->err, 0, ERR_WATCHDOG);
-                break;
-            }
-        }
-        if constexpr (TAG) flush_tagged();
-        // drain outstanding TMA stages before the CTA's shared memory is released
-        for (uint32_t spins = 0; landed_j < stg_j && spins < (1u << 26); ++spins) {
-            if (mbar_try_wait(&bar[landed_j % NST], (landed_j / NST) & 1u)) landed_j++;
-        }
-        if (P.flags & RS_FLAG_STATS) {
-            if (lane < K + 2) {
-                uint32_t a = 0, b = 0, c = 0, d = 0;
-#pragma unroll
-                for (int n = 0; n < K + 2; ++n)
-                    if (lane == n) { a = nd[n]; b = nf[n]; c = ni[n]; d = ns[n]; }
-                unsigned long long *S = P.stats + 4 * lane;
-                if (a) atomicAdd(S + 0, (unsigned long long)a);
-                if (b) atomicAdd(S + 1, (unsigned long long)b);
-                if (c) atomicAdd(S + 2, (unsigned long long)c);
-                if (d) atomicAdd(S + 3, (unsigned long long)d);
-            }
-        }
-    }
-};
-
-template <int K, int AGG, bool TAG>
-__global__ void __launch_bounds__(WPB * 32) k_pipeline(const __grid_constant__ KParams P) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    using PP = Pipe<K, AGG, TAG>;
-    uint8_t *mine = smem + (size_t)warp * PP::smem_bytes(P.qcap, P.scap);
-    if (P.hdr->err) return;
-    PP pipe(P, mine, lane);
-    pipe.run();
-}
+#include "rs_pipe.cuh"
 
 // ------------------------------------------------------------ host side
 thread_local std::string g_err;
@@ -929,7 +309,7 @@ rs_status rs_config_default(rs_config *cfg) {
     if (!cfg) return fail(RS_ERR_INVALID_ARG, "cfg is NULL");
     cfg->strategy = RS_STRATEGY_SIGNAL;
     cfg->simd_width = W;
-    cfg->queue_cap = 2 * W;
+    cfg->queue_cap = 8 * W;    // SPEC default 8w
     cfg->signal_cap = 128;
     cfg->grid = 0;
     cfg->chunk = 0;
@@ -967,7 +347,7 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
         return fail(RS_ERR_INVALID_ARG, "bad strategy");
     if (cfg.simd_width == 0) cfg.simd_width = W;
     if (cfg.simd_width != (uint32_t)W) return fail(RS_ERR_UNSUPPORTED, "only simd_width 128 is built");
-    if (cfg.queue_cap == 0) cfg.queue_cap = 2 * W;
+    if (cfg.queue_cap == 0) cfg.queue_cap = 8 * W;
     if (cfg.signal_cap == 0) cfg.signal_cap = 128;
     if (!is_pow2(cfg.queue_cap) || cfg.queue_cap < 2 * W || cfg.queue_cap > 65536)
         return fail(RS_ERR_UNSUPPORTED, "queue_cap must be a power of 2 in [256, 65536]");
@@ -1050,18 +430,28 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
 
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return fail(RS_ERR_CUDA, "cudaGetDevice failed");
-    const uint32_t cta_smem = L.inst_bytes * WPB;
     if (p->device != dev || p->grid == 0) {
+        // Pick warps-per-CTA (instances per CTA) to pack the most instances per SM.
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (cudaFuncSetAttribute(L.main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cta_smem) != cudaSuccess)
-            return fail(RS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(cudaGetLastError()));
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.main, WPB * 32, cta_smem);
-        if (per_sm < 1) return fail(RS_ERR_UNSUPPORTED, "pipeline does not fit on an SM (queue/signal capacities too large)");
-        p->grid = p->cfg.grid > 0 ? p->cfg.grid : sms * per_sm;
+        int best = 0, best_w = 1;
+        for (int w = WPB; w >= 1; w >>= 1) {
+            const uint32_t bytes = L.inst_bytes * w;
+            if (cudaFuncSetAttribute(L.main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.main, w * 32, bytes);
+            if (per_sm * w > best) { best = per_sm * w; best_w = w; }
+        }
+        if (best < 1) return fail(RS_ERR_UNSUPPORTED, "pipeline does not fit on an SM (queue/signal capacities too large)");
+        p->wpb = best_w;
+        const int blocks = best / best_w;
+        p->grid = p->cfg.grid > 0 ? p->cfg.grid : sms * blocks;
         p->device = dev;
     }
+    const uint32_t cta_smem = L.inst_bytes * p->wpb;
     cudaFuncSetAttribute(L.main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cta_smem);
 
     KParams K;
@@ -1096,7 +486,7 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
     if (timing) cudaEventRecord(p->ev[0], stream);
     L.pre<<<pre_blocks, 256, 0, stream>>>(K, 4 * (p->nst + 2));
     if (timing) cudaEventRecord(p->ev[1], stream);
-    L.main<<<p->grid, WPB * 32, cta_smem, stream>>>(K);
+    L.main<<<p->grid, p->wpb * 32, cta_smem, stream>>>(K);
     if (timing) cudaEventRecord(p->ev[2], stream);
     int fix_blocks = (int)std::min<long long>((wl.max_chunks + 255) / 256, 148 * 8);
     L.fix<<<std::max(fix_blocks, 1), 256, 0, stream>>>(K);

@@ -1,0 +1,803 @@
+// rs_pipe.cuh — one pipeline INSTANCE per warp (included by rs.cu).
+//
+// Nodes 0 = ENUMERATE, 1..K = FILTER/TRANSFORM, K+1 = AGGREGATE; edge e joins
+// node e -> e+1 with a data queue and, for the signal strategy, a
+// signal queue.  See rs.cu's header comment for the model; the
+// citations below point at the PAPER.md lines each step realises.
+#pragma once
+
+// ------------------------------------------------- filter / transform ops
+// isGood() / push() bodies (Fig. 5), specialised per op so the
+// full-ensemble path carries no per-item dispatch (readings A13/A14).
+struct OpHash {
+    uint32_t a, t;
+    __device__ __forceinline__ bool operator()(uint32_t &v) const { return ((v * a) >> 24) < t; }
+};
+struct OpLt {
+    uint32_t b;
+    bool all;
+    __device__ __forceinline__ bool operator()(uint32_t &v) const { return all || v < b; }
+};
+struct OpClass {
+    const uint32_t *tbl;
+    __device__ __forceinline__ bool operator()(uint32_t &v) const { return (tbl[(v & 0xffu) >> 5] >> (v & 31u)) & 1u; }
+};
+struct OpScale {
+    float s;
+    __device__ __forceinline__ bool operator()(uint32_t &v) const {
+        v = __float_as_uint(__fmul_rn(s, __uint_as_float(v)));
+        return true;
+    }
+};
+struct OpAffine {
+    uint32_t a, b;
+    __device__ __forceinline__ bool operator()(uint32_t &v) const {
+        v = v * a + b;
+        return true;
+    }
+};
+
+struct Chunk {
+    int32_t k;             // chunk id (-1 = empty slot)
+    long long beg, end;    // element range [beg, end)
+    uint32_t pos;          // Q0 queue position of element `beg`
+    uint32_t fr0, fr1;     // regions starting in the chunk: [fr0, fr1)
+    bool head;             // chunk starts inside region fr0-1 (a head part)
+};
+
+template <int K, int AGG, bool TAG>
+struct Pipe {
+    using AT = AggT<AGG>;
+    using A = typename AT::A;
+    static constexpr int SBLK = TAG ? 256 : 512;     // elements per TMA stage
+    static constexpr int RING0 = NST * SBLK;         // Q0 ring capacity (items)
+
+    const KParams &P;
+    const int lane;
+    const uint32_t lt;             // %lanemask_lt
+    // shared-memory rings
+    uint8_t *base;                 // this instance's shared-memory window
+    uint64_t *bar;                 // [NST] TMA stage barriers
+    uint32_t qmask, smask, qcap, scap;
+
+    // Edge e (node e -> node e+1).  Kept as named scalars (not arrays) so the
+    // whole state lives in registers.
+    struct EdgeS {
+        uint32_t qh, qt;       // data queue head/tail (monotone positions)
+        uint32_t sh, st;       // signal queue head/tail
+        uint32_t sent;         // sender: items emitted since last signal
+        uint32_t cur;          // receiver: current credit counter
+        bool xfer;             // the head signal's credit already moved into cur
+    };
+    EdgeS E0, E1, E2, E3, E4;
+    // per-node stats: ensembles, full ensembles, items, signals
+    struct NodeS { uint32_t nd, nf, ni, ns; };
+    NodeS N0, N1, N2, N3, N4, N5;
+
+    template <int e> __device__ __forceinline__ EdgeS &E() {
+        static_assert(e >= 0 && e <= 4, "edge index");
+        if constexpr (e == 0) return E0; else if constexpr (e == 1) return E1; else if constexpr (e == 2) return E2;
+        else if constexpr (e == 3) return E3; else return E4;
+    }
+    template <int e> __device__ __forceinline__ const EdgeS &E() const {
+        return const_cast<Pipe *>(this)->template E<e>();
+    }
+    template <int n> __device__ __forceinline__ NodeS &N() {
+        static_assert(n >= 0 && n <= 5, "node index");
+        if constexpr (n == 0) return N0; else if constexpr (n == 1) return N1; else if constexpr (n == 2) return N2;
+        else if constexpr (n == 3) return N3; else if constexpr (n == 4) return N4; else return N5;
+    }
+    // ring addresses: Q0 (RING0 items) then Q_1..Q_K (qcap items), each followed
+    // by its tag ring in the tagged strategy, then the signal rings.
+    template <int e> __device__ __forceinline__ uint32_t *Q() const {
+        if constexpr (e == 0) return reinterpret_cast<uint32_t *>(base + 128);
+        else return reinterpret_cast<uint32_t *>(base + 128 + RING0 * 4 * (TAG ? 2 : 1) + (e - 1) * qcap * 4 * (TAG ? 2 : 1));
+    }
+    template <int e> __device__ __forceinline__ uint32_t *T() const {
+        if constexpr (!TAG) return nullptr;
+        else return Q<e>() + (e == 0 ? RING0 : qcap);
+    }
+    template <int e> __device__ __forceinline__ uint2 *S() const {
+        return reinterpret_cast<uint2 *>(base + 128 + RING0 * 4 * (TAG ? 2 : 1) + K * qcap * 4 * (TAG ? 2 : 1)) + e * scap;
+    }
+
+    Chunk F0, F1;                      // chunk being enumerated, chunk staged next
+    bool claims_done, enum_done;
+    uint32_t stg_j, landed_j;          // TMA stages issued / known landed
+    uint32_t pidx;                     // next part of F0 to enumerate
+    bool begun;                        // Begin of part pidx already emitted
+    // part-info cache: lane i holds part pc_base + i of F0
+    uint32_t pc_base;
+    bool pc_valid;
+    long long pc_ps, pc_pe;
+    uint32_t pc_key;
+    // aggregate state
+    A acc;             // per-lane partial accumulator
+    uint32_t akey;     // tagged: key of the running (carry) region; 0xffffffff = none
+    A carry;           // tagged: uniform partial of the carry region
+    long long base0, offR, off0;
+    uint32_t nchunks;
+
+    __device__ __forceinline__ Pipe(const KParams &p, uint8_t *smem, int lane_)
+        : P(p), lane(lane_), lt(lanemask_lt()) {
+        qcap = P.qcap;
+        scap = P.scap;
+        qmask = qcap - 1;
+        smask = scap - 1;
+        base = smem;
+        bar = reinterpret_cast<uint64_t *>(smem);
+        E0 = E1 = E2 = E3 = E4 = EdgeS{0u, 0u, 0u, 0u, 0u, 0u, false};
+        N0 = N1 = N2 = N3 = N4 = N5 = NodeS{0u, 0u, 0u, 0u};
+        F0.k = F1.k = -1;
+        claims_done = enum_done = false;
+        stg_j = landed_j = 0;
+        pidx = 0;
+        begun = false;
+        pc_valid = false;
+        pc_base = 0;
+        acc = AT::id();
+        carry = AT::id();
+        akey = 0xffffffffu;
+        base0 = P.hdr->base0;
+        offR = P.hdr->offR;
+        off0 = P.hdr->off0;
+        nchunks = P.hdr->nchunks;
+    }
+
+    __host__ __device__ static constexpr uint32_t smem_bytes(uint32_t qcap, uint32_t scap) {
+        return 128 + RING0 * 4 * (TAG ? 2 : 1) + K * qcap * 4 * (TAG ? 2 : 1) + (TAG ? 0 : (K + 1) * scap * 8);
+    }
+
+    // ---------------------------------------------------------- chunks
+    __device__ __forceinline__ void load_chunk(Chunk &c, int32_t k, uint32_t pos) const {
+        c.k = k;
+        c.beg = (k == 0) ? off0 : base0 + (long long)k * P.C;
+        long long e = base0 + (long long)(k + 1) * P.C;
+        c.end = e > offR ? offR : e;
+        c.pos = pos;
+        c.fr0 = P.chunk_fr[k];
+        c.fr1 = P.chunk_fr[k + 1];
+        c.head = (k > 0) && (P.off[c.fr0] > c.beg);
+    }
+    __device__ __forceinline__ static uint32_t flen(const Chunk &c) { return (uint32_t)(c.end - c.beg); }
+
+    // Claim the next chunk of the parent stream (atomics, no locks).
+    __device__ __forceinline__ int32_t claim() {
+        uint32_t k = 0;
+        if (lane == 0) k = atomicAdd(&P.hdr->claim, 1u);
+        k = __shfl_sync(kFull, k, 0);
+        return k < nchunks ? (int32_t)k : -1;
+    }
+
+    // Issue TMA stage stg_j (positions [j*SBLK, (j+1)*SBLK)) from chunk c.
+    __device__ __forceinline__ void issue_stage(const Chunk &c) {
+        const uint32_t j = stg_j;
+        const uint32_t p0 = j * SBLK;
+        const uint32_t n = min((uint32_t)SBLK, c.pos + flen(c) - p0);
+        const long long src = c.beg + (long long)p0 - (long long)c.pos;   // 16-byte aligned element index
+        uint32_t *dst = Q<0>() + (p0 & (RING0 - 1));
+        uint64_t *b = &bar[j % NST];
+        const long long lim = (P.n_elems - src) & ~3ll;     // whole 16-byte blocks inside the array
+        const uint32_t ntma = (uint32_t)min((long long)((n + 3u) & ~3u), lim);
+        // tail elements that a 16-byte copy cannot reach without overrunning n_elems
+        const int tail = (int)n - (int)ntma;
+        if (tail > 0 && lane < tail)
+            dst[ntma + lane] = __ldg(reinterpret_cast<const uint32_t *>(P.elems) + src + ntma + lane);
+        __syncwarp();
+        if (lane == 0) {
+            fence_proxy_async();
+            if (ntma) {
+                mbar_arrive_expect_tx(b, ntma * 4u);
+                tma_load_1d(dst, P.elems + src * 4, ntma * 4u, b);
+            } else {
+                mbar_arrive(b);
+            }
+        }
+        stg_j = j + 1;
+    }
+
+    // Keep the Q0 ring full: prefetch element blocks ahead of the enumerate node.
+    __device__ __forceinline__ void refill() {
+        for (;;) {
+            if ((stg_j + 1) * (uint32_t)SBLK > E<0>().qh + RING0) return;   // ring slots still in use
+            const uint32_t sp = stg_j * SBLK;
+            if (F0.k >= 0 && sp < F0.pos + flen(F0)) { issue_stage(F0); continue; }
+            if (F1.k >= 0 && sp < F1.pos + flen(F1)) { issue_stage(F1); continue; }
+            if (F1.k >= 0 || claims_done) return;
+            const int32_t k = claim();
+            if (k < 0) { claims_done = true; return; }
+            if (F0.k < 0) {
+                const uint32_t pos = (k == 0) ? (uint32_t)(off0 - base0) : sp;
+                if (k == 0 && stg_j == 0) E<0>().qh = E<0>().qt = pos;
+                load_chunk(F0, k, pos);
+                pidx = 0;
+                begun = false;
+                pc_valid = false;
+            } else {
+                load_chunk(F1, k, F0.pos + flen(F0));
+            }
+        }
+    }
+
+    __device__ __forceinline__ void shift() {
+        F0 = F1;
+        F1.k = -1;
+        pidx = 0;
+        begun = false;
+        pc_valid = false;
+    }
+
+    // ------------------------------------------------------ enumerate
+    // Part qi of chunk F0: [start, end) elements and its key (region id, or a
+    // partial slot for the chunk's head part / a tail part crossing the chunk end).
+    __device__ __forceinline__ void part_info(uint32_t qi, bool valid, long long &ps, long long &pe, uint32_t &key) const {
+        ps = pe = F0.end;
+        key = 0;
+        if (!valid) return;
+        if (F0.head && qi == 0) {
+            ps = F0.beg;
+            const long long e = P.off[F0.fr0];
+            pe = e < F0.end ? e : F0.end;
+            key = SLOT | (uint32_t)(2 * F0.k);
+        } else {
+            const uint32_t r = F0.fr0 + qi - (F0.head ? 1u : 0u);
+            ps = P.off[r];
+            const long long e = P.off[r + 1];
+            if (e > F0.end) { pe = F0.end; key = SLOT | (uint32_t)(2 * F0.k + 1); }
+            else { pe = e; key = r; }
+        }
+    }
+
+    // Sender rule for one signal on edge e: S empty -> |Q|;
+    // otherwise items emitted since the tail signal.  Resets the counter.
+    template <int e>
+    __device__ __forceinline__ void push_signal(uint32_t key, bool end, uint32_t credit_rule2) {
+        const uint32_t credit = (E<e>().sh == E<e>().st) ? (E<e>().qt - E<e>().qh) : credit_rule2;
+        if (lane == 0) S<e>()[E<e>().st & smask] = make_uint2(key, credit | (end ? END_BIT : 0u));
+        E<e>().st += 1;
+        E<e>().sent = 0;
+    }
+
+    // One enumerate firing (resumable mid-region):
+    // emit F0's parts -- Begin, element indices (as staged element values),
+    // End -- as far as staged data and signal space allow.  Up to 32 parts are
+    // handled per step, one per lane, with warp scans over their counts.
+    __device__ __forceinline__ bool enumerate() {
+        bool prog = false;
+        refill();
+        for (;;) {
+            if (F0.k < 0) {
+                if (F1.k >= 0) { shift(); continue; }
+                if (claims_done) enum_done = true;
+                return prog;
+            }
+            const uint32_t np = (F0.head ? 1u : 0u) + (F0.fr1 - F0.fr0);
+            if (pidx >= np) {            // chunk fully enumerated
+                shift();
+                refill();
+                prog = true;
+                continue;
+            }
+            const uint32_t lim_pos = min(stg_j * (uint32_t)SBLK, F0.pos + flen(F0));
+            const uint32_t avail = lim_pos - E<0>().qt;
+            if (!pc_valid || pidx >= pc_base + 32) {
+                pc_base = pidx;
+                pc_valid = true;
+                part_info(pidx + lane, pidx + lane < np, pc_ps, pc_pe, pc_key);
+            }
+            const uint32_t d = pidx - pc_base;
+            const long long e_next = F0.beg + (long long)(E<0>().qt - F0.pos);
+            if (avail == 0 && (TAG || begun)) {
+                // cheap exit: the current part still has items but nothing is staged
+                const long long pe0 = __shfl_sync(kFull, pc_pe, d);
+                if (pe0 > e_next) return prog;
+            }
+            long long ps = __shfl_down_sync(kFull, pc_ps, d);
+            long long pe = __shfl_down_sync(kFull, pc_pe, d);
+            uint32_t key = __shfl_down_sync(kFull, pc_key, d);
+            const bool valid = (lane + d < 32) && (pidx + lane < np);
+            if (!valid) ps = pe = F0.end;
+            if (lane == 0 && ps < e_next) ps = e_next;     // resume inside part pidx
+            const uint32_t cnt = (uint32_t)(pe - ps);
+            uint32_t cum = cnt;
+            const uint32_t sig = TAG ? 0u : ((lane == 0 && begun) ? 1u : 2u);
+            uint32_t scum = sig;
+#pragma unroll
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const uint32_t o = __shfl_up_sync(kFull, cum, dd);
+                const uint32_t so = __shfl_up_sync(kFull, scum, dd);
+                if (lane >= dd) { cum += o; scum += so; }
+            }
+            const uint32_t sfree = TAG ? 0xffffffffu : scap - (E<0>().st - E<0>().sh);
+            const bool fits = valid && (cum <= avail) && (scum <= sfree);
+            const uint32_t m = __popc(__ballot_sync(kFull, fits));
+            if (m > 0) {
+                const uint32_t tot = __shfl_sync(kFull, cum, m - 1);
+                if constexpr (!TAG) {
+                    // Begin_i, End_i of parts 0..m-1 in stream order.
+                    const bool empty_at_start = (E<0>().sh == E<0>().st);
+                    const uint32_t qlen0 = E<0>().qt - E<0>().qh;
+                    const uint32_t sexcl = scum - sig;
+                    if (lane < (int)m) {
+                        uint32_t slot = E<0>().st + sexcl;
+                        if (!(lane == 0 && begun)) {
+                            // first signal of the step: rule (1) if S was empty, else
+                            // rule (2) (items since the previous signal); later Begins
+                            // follow an End directly: credit 0.
+                            const uint32_t c = (lane == 0) ? (empty_at_start ? qlen0 : E<0>().sent) : 0u;
+                            S<0>()[slot & smask] = make_uint2(key, c);
+                            slot++;
+                        }
+                        // End_i: items of part i since its Begin (rule 2), or rule (1) when
+                        // part 0 began earlier and S has since been drained by the receiver.
+                        uint32_t c = cnt;
+                        if (lane == 0 && begun) c = empty_at_start ? (qlen0 + cnt) : (E<0>().sent + cnt);
+                        S<0>()[slot & smask] = make_uint2(key, c | END_BIT);
+                    }
+                    const uint32_t nsig = __shfl_sync(kFull, scum, m - 1);
+                    E<0>().st += nsig;
+                    N<0>().ns += nsig;
+                    E<0>().sent = 0;
+                } else {
+                    write_tags(m, cum, cnt, key, tot);
+                }
+                E<0>().qt += tot;
+                N<0>().ni += tot;
+                pidx += m;
+                begun = false;
+                prog = true;
+                __syncwarp();
+                continue;
+            }
+            // Part pidx does not fit whole: emit what we can of it (resumable).
+            const uint32_t key0 = __shfl_sync(kFull, key, 0);
+            const uint32_t cnt0 = __shfl_sync(kFull, cnt, 0);
+            bool did = false;
+            if constexpr (!TAG) {
+                if (!begun) {
+                    if (scap - (E<0>().st - E<0>().sh) == 0) return prog;
+                    push_signal<0>(key0, false, E<0>().sent);
+                    N<0>().ns++;
+                    begun = true;
+                    did = true;
+                }
+            }
+            const uint32_t k = min(avail, cnt0);
+            if (k > 0) {
+                if constexpr (TAG) write_tags_uniform(key0, k);
+                E<0>().qt += k;
+                E<0>().sent += k;
+                N<0>().ni += k;
+                did = true;
+            }
+            if constexpr (!TAG) {
+                if (k == cnt0 && scap - (E<0>().st - E<0>().sh) > 0) {
+                    push_signal<0>(key0, true, E<0>().sent);
+                    N<0>().ns++;
+                    pidx++;
+                    begun = false;
+                    did = true;
+                }
+            } else {
+                if (k == cnt0) { pidx++; did = true; }
+            }
+            __syncwarp();
+            prog |= did;
+            if (!did) return prog;
+        }
+    }
+
+    // Tagged enumerate: every emitted item carries its parent's key
+    // (P:258-261).  Positions E<0>().qt .. E<0>().qt+tot-1 belong to parts
+    // 0..m-1 of this step (lane i holds part i's inclusive end `cum`).
+    __device__ __forceinline__ void write_tags(uint32_t m, uint32_t cum, uint32_t cnt, uint32_t key, uint32_t tot) {
+        if (m == 1 || __shfl_sync(kFull, cnt, 0) == tot) {
+            write_tags_uniform(__shfl_sync(kFull, key, 0), tot);
+            return;
+        }
+        const uint32_t excl = cum - cnt;
+        for (uint32_t base = 0; base < tot; base += 32) {
+            const uint32_t rel = base + lane;
+            int lo = 0;      // largest part i < m with excl_i <= rel
+#pragma unroll
+            for (int step = 16; step >= 1; step >>= 1) {
+                const int cand = lo + step;
+                const uint32_t ex = __shfl_sync(kFull, excl, cand < 32 ? cand : 31);
+                if (cand < (int)m && ex <= rel) lo = cand;
+            }
+            const uint32_t k = __shfl_sync(kFull, key, lo);
+            if (rel < tot) T<0>()[(E<0>().qt + rel) & (RING0 - 1)] = k;
+        }
+    }
+    __device__ __forceinline__ void write_tags_uniform(uint32_t key, uint32_t k) {
+        for (uint32_t i = lane; i < k; i += 32) T<0>()[(E<0>().qt + i) & (RING0 - 1)] = key;
+    }
+
+    // ---------------------------------------------------------- stages
+    __device__ __forceinline__ uint32_t landed_pos() {
+        while (landed_j < stg_j && mbar_test(&bar[landed_j % NST], (landed_j / NST) & 1u)) landed_j++;
+        return landed_j * (uint32_t)SBLK;
+    }
+
+    // Receiver admissible count on edge e, applying rule (2b).
+    template <int e>
+    __device__ __forceinline__ uint32_t admissible(bool &spend) {
+        spend = E<e>().sh != E<e>().st;
+        const uint32_t ql = E<e>().qt - E<e>().qh;
+        if (!spend) return ql;
+        if (E<e>().cur == 0 && !E<e>().xfer) {
+            const uint32_t c = S<e>()[E<e>().sh & smask].y & ~END_BIT;
+            if (c > 0) { E<e>().cur = c; E<e>().xfer = true; }
+        }
+        return min(ql, E<e>().cur);
+    }
+
+    // Full ensembles of a FILTER/TRANSFORM node, specialised per op.  Item t
+    // of an ensemble lives in lane t%32, slot t/32; loads are issued first
+    // (4-way ILP), then the predicates, then the stable ballot/popc
+    // compaction into the output queue (push).
+    template <int n, class Op>
+    __device__ __forceinline__ void filter_full(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
+                                                uint32_t nens, const Op op) {
+        uint32_t *out = Q<n>();
+        uint32_t *tout = T<n>();
+        uint32_t tl = E<n>().qt;
+        for (uint32_t k = 0; k < nens; ++k, h += W) {
+            uint32_t v[IPL], tg[IPL];
+            bool keep[IPL];
+            if (((h & imask) + W) <= imask + 1) {          // ensemble does not wrap the ring
+                const uint32_t *src = in + (h & imask) + lane;
+#pragma unroll
+                for (int j = 0; j < IPL; ++j) v[j] = src[32 * j];
+                if constexpr (TAG) {
+                    const uint32_t *ts = tin + (h & imask) + lane;
+#pragma unroll
+                    for (int j = 0; j < IPL; ++j) tg[j] = ts[32 * j];
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < IPL; ++j) v[j] = in[(h + 32 * j + lane) & imask];
+                if constexpr (TAG) {
+#pragma unroll
+                    for (int j = 0; j < IPL; ++j) tg[j] = tin[(h + 32 * j + lane) & imask];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < IPL; ++j) keep[j] = op(v[j]);
+            uint32_t mk[IPL];
+#pragma unroll
+            for (int j = 0; j < IPL; ++j) mk[j] = __ballot_sync(kFull, keep[j]);
+            if (((tl & qmask) + W) <= qcap) {              // output does not wrap the ring
+                uint32_t *dst = out + (tl & qmask);
+                uint32_t *tdst = TAG ? tout + (tl & qmask) : nullptr;
+                uint32_t off = 0;
+#pragma unroll
+                for (int j = 0; j < IPL; ++j) {
+                    if (keep[j]) {
+                        const uint32_t o = off + __popc(mk[j] & lt);
+                        dst[o] = v[j];
+                        if constexpr (TAG) tdst[o] = tg[j];
+                    }
+                    off += __popc(mk[j]);
+                }
+                tl += off;
+            } else {
+#pragma unroll
+                for (int j = 0; j < IPL; ++j) {
+                    if (keep[j]) {
+                        const uint32_t pos = (tl + __popc(mk[j] & lt)) & qmask;
+                        out[pos] = v[j];
+                        if constexpr (TAG) tout[pos] = tg[j];
+                    }
+                    tl += __popc(mk[j]);
+                }
+            }
+        }
+        E<n>().sent += tl - E<n>().qt;
+        E<n>().qt = tl;
+    }
+
+    // Full ensembles of the aggregate (signal strategy: one region per
+    // ensemble, P:495-499 -> plain per-lane accumulation, a::run P:533).
+    __device__ __forceinline__ void agg_full(const uint32_t *in, uint32_t imask, uint32_t h, uint32_t nens) {
+        for (uint32_t k = 0; k < nens; ++k, h += W) {
+            uint32_t v[IPL];
+            if (((h & imask) + W) <= imask + 1) {
+                const uint32_t *src = in + (h & imask) + lane;
+#pragma unroll
+                for (int j = 0; j < IPL; ++j) v[j] = src[32 * j];
+            } else {
+#pragma unroll
+                for (int j = 0; j < IPL; ++j) v[j] = in[(h + 32 * j + lane) & imask];
+            }
+#pragma unroll
+            for (int j = 0; j < IPL; ++j) acc = AT::comb(acc, AT::lift(v[j]));
+        }
+    }
+
+    template <int n>
+    __device__ __forceinline__ void run_full(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
+                                             uint32_t nens) {
+        if constexpr (n == K + 1) {
+            if constexpr (!TAG) {
+                agg_full(in, imask, h, nens);
+            } else {
+                for (uint32_t k = 0; k < nens; ++k) agg_tagged(in, tin, imask, h + k * W, W);
+            }
+        } else {
+            const StageP &sp = P.st[n - 1];
+            switch (sp.op) {
+                case RS_OP_HASH_LT: filter_full<n>(in, tin, imask, h, nens, OpHash{sp.a, sp.b}); break;
+                case RS_OP_LT_U32: filter_full<n>(in, tin, imask, h, nens, OpLt{sp.b, sp.table[0] != 0}); break;
+                case RS_OP_CLASS: filter_full<n>(in, tin, imask, h, nens, OpClass{sp.table}); break;
+                case RS_OP_SCALE_F32: filter_full<n>(in, tin, imask, h, nens, OpScale{__uint_as_float(sp.a)}); break;
+                default: filter_full<n>(in, tin, imask, h, nens, OpAffine{sp.a, sp.b}); break;
+            }
+            __syncwarp();
+        }
+    }
+
+    // Fire node n (1..K+1) repeatedly while it can make progress: data phase,
+    // then signal phase, full-first (A8).
+    template <int n>
+    __device__ __forceinline__ bool fire(bool drained) {
+        constexpr int ei = n - 1;          // input edge
+        constexpr bool AGGN = (n == K + 1);
+        const uint32_t imask = (ei == 0) ? (RING0 - 1) : qmask;
+        const uint32_t *in = Q<ei>();
+        const uint32_t *tin = T<ei>();
+        bool prog = false;
+        uint32_t ready_lim = 0;
+        if (ei == 0) ready_lim = landed_pos();
+        for (;;) {
+            bool spend;
+            const uint32_t a = admissible<ei>(spend);
+            uint32_t ar = a;
+            if (ei == 0) {
+                // only items whose TMA stage has landed may be read
+                if ((int)(ready_lim - E<0>().qh) < (int)ar) ready_lim = landed_pos();
+                const int rdy = (int)(ready_lim - E<0>().qh);
+                ar = rdy <= 0 ? 0u : min(ar, (uint32_t)rdy);
+            }
+            uint32_t space = 0xffffffffu;
+            if constexpr (!AGGN) space = qcap - (E<n>().qt - E<n>().qh);
+            const uint32_t lim = min(ar, space);
+            if (lim >= (uint32_t)W) {
+                // as many full ensembles as the credit / data / space allow
+                const uint32_t nens = lim / W;
+                run_full<n>(in, tin, imask, E<ei>().qh, nens);
+                E<ei>().qh += nens * W;
+                if (spend) E<ei>().cur -= nens * W;
+                N<n>().nd += nens;
+                N<n>().nf += nens;
+                N<n>().ni += nens * W;
+                prog = true;
+                continue;
+            }
+            const uint32_t e = lim;
+            bool ok = e > 0;
+            if (ok) {
+                const bool bounded = spend && e == E<ei>().cur;        // ensemble <= credit
+                const bool dr = drained && e == a;
+                ok = bounded || dr;
+            }
+            if (ok) {
+                run_partial<n>(in, tin, imask, E<ei>().qh, e);
+                E<ei>().qh += e;
+                if (spend) E<ei>().cur -= e;
+                N<n>().nd++;
+                N<n>().ni += e;
+                prog = true;
+                continue;
+            }
+            // signal phase: only with the counter at 0
+            if constexpr (TAG) break;
+            if (!spend || E<ei>().cur != 0) break;
+            const uint2 hs = S<ei>()[E<ei>().sh & smask];
+            if (!E<ei>().xfer && (hs.y & ~END_BIT) > 0) {
+                E<ei>().cur = hs.y & ~END_BIT;
+                E<ei>().xfer = true;
+                continue;
+            }
+            if constexpr (!AGGN) {
+                if (scap - (E<n>().st - E<n>().sh) == 0) break;
+            }
+            E<ei>().sh++;
+            E<ei>().xfer = false;
+            N<n>().ns++;
+            prog = true;
+            const bool is_end = (hs.y & END_BIT) != 0;
+            if constexpr (AGGN) {
+                if (!is_end) {               // a::begin: acc = identity
+                    acc = AT::id();
+                } else {                     // a::end: push(acc)
+                    const A v = warp_reduce<AT>(acc);
+                    if (lane == 0) store_key(hs.x, v);
+                    acc = AT::id();
+                }
+            } else {
+                push_signal<n>(hs.x, is_end, E<n>().sent);   // forwarded with a fresh credit
+            }
+        }
+        __syncwarp();
+        return prog;
+    }
+
+    __device__ __forceinline__ void store_key(uint32_t key, A v) {
+        if (key & SLOT) AT::store(P.part0, P.part1, key & ~SLOT, v);
+        else AT::store(P.out0, P.out1, key, v);
+    }
+
+    // One partial ensemble (signal-bounded or at the drained tail).
+    template <int n>
+    __device__ __forceinline__ void run_partial(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
+                                                uint32_t e) {
+        if constexpr (n == K + 1) {
+            if constexpr (!TAG) {
+#pragma unroll
+                for (int j = 0; j < IPL; ++j) {
+                    const uint32_t idx = j * 32 + lane;
+                    if (idx < e) acc = AT::comb(acc, AT::lift(in[(h + idx) & imask]));
+                }
+            } else {
+                agg_tagged(in, tin, imask, h, e);
+            }
+        } else {
+            const StageP &sp = P.st[n - 1];
+            uint32_t *out = Q<n>();
+            uint32_t *tout = T<n>();
+            uint32_t tl = E<n>().qt;
+#pragma unroll
+            for (int j = 0; j < IPL; ++j) {
+                const uint32_t idx = j * 32 + lane;
+                const bool act = idx < e;
+                uint32_t v = act ? in[(h + idx) & imask] : 0u;
+                uint32_t tg = 0;
+                if constexpr (TAG) tg = act ? tin[(h + idx) & imask] : 0u;
+                const bool keep = act && stage_apply(sp, v);
+                const uint32_t mk = __ballot_sync(kFull, keep);   // stable compaction
+                if (keep) {
+                    const uint32_t pos = (tl + __popc(mk & lt)) & qmask;
+                    out[pos] = v;
+                    if constexpr (TAG) tout[pos] = tg;
+                }
+                tl += __popc(mk);
+            }
+            E<n>().sent += tl - E<n>().qt;
+            E<n>().qt = tl;
+            __syncwarp();
+        }
+    }
+
+    // Region-id-keyed segmented reduction with a carry across ensembles
+    // (tagged aggregate).  Ensembles may mix regions.
+    __device__ __forceinline__ void agg_tagged(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
+                                               uint32_t e) {
+#pragma unroll
+        for (int j = 0; j < IPL; ++j) {
+            const int cntj = (int)e - j * 32;
+            if (cntj <= 0) break;
+            const bool act = lane < cntj;
+            const uint32_t idx = j * 32 + lane;
+            const uint32_t key = act ? tin[(h + idx) & imask] : 0xffffffffu;
+            const A val = act ? AT::lift(in[(h + idx) & imask]) : AT::id();
+            if (__all_sync(kFull, !act || key == akey)) {
+                acc = AT::comb(acc, val);      // fast path: the whole slice continues the carry region
+                continue;
+            }
+            // fold per-lane partials of the carry into `carry`
+            carry = AT::comb(carry, warp_reduce<AT>(acc));
+            acc = AT::id();
+            uint32_t prev = __shfl_up_sync(kFull, key, 1);
+            if (lane == 0) prev = akey;
+            const bool head = act && key != prev;
+            const uint32_t hm = __ballot_sync(kFull, head);
+            const uint32_t le = hm & lanemask_le();
+            const int seg = le ? 31 - __clz(le) : -1;     // first lane of my segment (-1: carry segment)
+            A v = val;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const A o = AT::shfl_up(v, d);
+                if (lane - d >= seg && lane >= d) v = AT::comb(o, v);
+            }
+            if (seg < 0 && act) v = AT::comb(carry, v);
+            // the carry region ended exactly before this slice
+            if (lane == 0 && head && akey != 0xffffffffu) store_key(akey, carry);
+            const bool nexthead = (lane < 31) && ((hm >> (lane + 1)) & 1u);
+            if (act && nexthead) store_key(key, v);      // complete segment inside the slice
+            const int last = (cntj < 32 ? cntj : 32) - 1;   // last active lane of this slice
+            akey = __shfl_sync(kFull, key, last);
+            carry = AT::shfl(v, last);
+        }
+    }
+
+    __device__ __forceinline__ void flush_tagged() {
+        carry = AT::comb(carry, warp_reduce<AT>(acc));
+        acc = AT::id();
+        if (lane == 0 && akey != 0xffffffffu) store_key(akey, carry);
+        akey = 0xffffffffu;
+        carry = AT::id();
+    }
+
+    template <int k = 0>
+    __device__ __forceinline__ bool all_empty() const {
+        if constexpr (k > K) {
+            return true;
+        } else {
+            return (E<k>().qh == E<k>().qt) && (E<k>().sh == E<k>().st) && all_empty<k + 1>();
+        }
+    }
+
+    template <int n>
+    __device__ __forceinline__ bool fire_chain(bool drained) {
+        if constexpr (n > K + 1) {
+            return false;
+        } else {
+            const bool p = fire<n>(drained);
+            const bool dn = drained && (E<n - 1>().qh == E<n - 1>().qt) && (E<n - 1>().sh == E<n - 1>().st);
+            return fire_chain<n + 1>(dn) | p;
+        }
+    }
+
+    template <int n>
+    __device__ __forceinline__ void flush_stats() {
+        if constexpr (n < K + 2) {
+            if (lane == n) {
+                unsigned long long *S = P.stats + 4 * n;
+                if (N<n>().nd) atomicAdd(S + 0, (unsigned long long)N<n>().nd);
+                if (N<n>().nf) atomicAdd(S + 1, (unsigned long long)N<n>().nf);
+                if (N<n>().ni) atomicAdd(S + 2, (unsigned long long)N<n>().ni);
+                if (N<n>().ns) atomicAdd(S + 3, (unsigned long long)N<n>().ns);
+            }
+            flush_stats<n + 1>();
+        }
+    }
+
+    __device__ __forceinline__ void run() {
+        if (lane == 0)
+            for (int i = 0; i < NST; ++i) mbar_init(&bar[i], 1);
+        mbar_fence_init();
+        __syncwarp();
+        uint32_t idle = 0;
+        for (;;) {
+            bool prog = enumerate();
+            prog |= fire_chain<1>(enum_done);
+            if (enum_done && all_empty()) break;
+            if (prog) { idle = 0; continue; }
+            // nothing fireable: wait for the oldest in-flight TMA stage
+            if (landed_j < stg_j) {
+                uint32_t spins = 0;
+                while (!mbar_try_wait(&bar[landed_j % NST], (landed_j / NST) & 1u)) {
+                    if (++spins > (1u << 24)) break;
+                }
+                if (spins > (1u << 24)) {
+                    if (lane == 0) atomicCAS((int *)&P.hdr->err, 0, ERR_WATCHDOG);
+                    break;
+                }
+                continue;
+            }
+            if (++idle > 64) {
+                if (lane == 0) atomicCAS((int *)&P.hdr->err, 0, ERR_WATCHDOG);
+                break;
+            }
+        }
+        if constexpr (TAG) flush_tagged();
+        // drain outstanding TMA stages before the CTA's shared memory is released
+        for (uint32_t spins = 0; landed_j < stg_j && spins < (1u << 26); ++spins) {
+            if (mbar_try_wait(&bar[landed_j % NST], (landed_j / NST) & 1u)) landed_j++;
+        }
+        if (P.flags & RS_FLAG_STATS) flush_stats<0>();
+    }
+};
+
+template <int K, int AGG, bool TAG>
+__global__ void __launch_bounds__(WPB * 32, 1) k_pipeline(const __grid_constant__ KParams P) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    using PP = Pipe<K, AGG, TAG>;
+    uint8_t *mine = smem + (size_t)warp * PP::smem_bytes(P.qcap, P.scap);
+    if (P.hdr->err) return;
+    PP pipe(P, mine, lane);
+    pipe.run();
+}
