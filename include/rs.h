@@ -96,7 +96,10 @@ typedef struct {
 enum {
     RS_FLAG_STATS = 1u,      /* collect per-node occupancy counters (default on)     */
     RS_FLAG_VALIDATE = 2u,   /* device-check offsets monotone and <= n_elems          */
-    RS_FLAG_TIMING = 4u      /* record CUDA events around each kernel of a run        */
+    RS_FLAG_TIMING = 4u,     /* record CUDA events around each kernel of a run        */
+    RS_FLAG_SEQUENTIAL = 8u  /* one warp per instance firing one node at a time (the
+                                paper's per-processor scheduler) instead of
+                                the default warp-specialised instance (one warp per node) */
 };
 
 typedef struct {
@@ -171,7 +174,8 @@ rs_status rs_pipeline_stats(rs_pipeline *p, rs_node_stats *host_out, int n_nodes
 /* Read the device error word of the last run (synchronises `stream`).
  * Returns RS_ERR_PROTOCOL and sets *code (if non-NULL) when the device saw a
  * violated invariant: 1 = bad offsets (VALIDATE), 2 = watchdog (no progress),
- * 3 = signal queue overflow, 4 = unmatched End, 5 = queue overflow. */
+ * 3 = signal queue overflow, 4 = unmatched End, 5 = queue overflow,
+ * 7 = a receiver's readable limit fell behind its consumed position. */
 rs_status rs_pipeline_check(rs_pipeline *p, rs_stream stream, int32_t *code);
 
 /* Device time of the last run's kernels (needs RS_FLAG_TIMING; synchronises

@@ -45,7 +45,7 @@ constexpr int MAXK = 4;             // max FILTER/TRANSFORM stages
 constexpr int NST = 4;              // TMA stages in the Q0 ring
 constexpr int WPB = 4;              // warps (instances) per CTA
 
-enum : int32_t { ERR_OFFSETS = 1, ERR_WATCHDOG = 2, ERR_SIGFULL = 3, ERR_UNMATCHED = 4, ERR_QFULL = 5 };
+enum : int32_t { ERR_OFFSETS = 1, ERR_WATCHDOG = 2, ERR_SIGFULL = 3, ERR_UNMATCHED = 4, ERR_QFULL = 5, ERR_LIMIT = 7 };
 
 struct StageP {
     int32_t kind, op;
@@ -178,6 +178,7 @@ __global__ void k_fixup(KParams P) {
 
 // ---------------------------------------------------------- the pipeline
 #include "rs_pipe.cuh"
+#include "rs_ws.cuh"
 
 // ------------------------------------------------------------ host side
 thread_local std::string g_err;
@@ -226,6 +227,28 @@ KernelFn pick_k(int K) {
 }
 
 template <int AGG, bool TAG>
+KernelFn pick_ws(int K) {
+    switch (K) {
+        case 0: return k_pipeline_ws<0, AGG, TAG>;
+        case 1: return k_pipeline_ws<1, AGG, TAG>;
+        case 2: return k_pipeline_ws<2, AGG, TAG>;
+        case 3: return k_pipeline_ws<3, AGG, TAG>;
+        default: return k_pipeline_ws<4, AGG, TAG>;
+    }
+}
+
+template <int AGG, bool TAG>
+uint32_t smem_ws(int K, uint32_t qcap, uint32_t scap) {
+    switch (K) {
+        case 0: return WS<0, AGG, TAG>::smem_bytes(qcap, scap);
+        case 1: return WS<1, AGG, TAG>::smem_bytes(qcap, scap);
+        case 2: return WS<2, AGG, TAG>::smem_bytes(qcap, scap);
+        case 3: return WS<3, AGG, TAG>::smem_bytes(qcap, scap);
+        default: return WS<4, AGG, TAG>::smem_bytes(qcap, scap);
+    }
+}
+
+template <int AGG, bool TAG>
 uint32_t smem_for(int K, uint32_t qcap, uint32_t scap) {
     switch (K) {
         case 0: return Pipe<0, AGG, TAG>::smem_bytes(qcap, scap);
@@ -238,6 +261,8 @@ uint32_t smem_for(int K, uint32_t qcap, uint32_t scap) {
 
 struct Launch {
     KernelFn main;
+    KernelFn ws;
+    uint32_t ws_bytes;
     void (*pre)(KParams, int);
     void (*fix)(KParams);
     uint32_t inst_bytes;
@@ -248,6 +273,8 @@ template <int AGG>
 Launch launch_for(int K, bool tag, uint32_t qcap, uint32_t scap) {
     Launch L;
     L.main = tag ? pick_k<AGG, true>(K) : pick_k<AGG, false>(K);
+    L.ws = tag ? pick_ws<AGG, true>(K) : pick_ws<AGG, false>(K);
+    L.ws_bytes = tag ? smem_ws<AGG, true>(K, qcap, scap) : smem_ws<AGG, false>(K, qcap, scap);
     L.pre = k_prepass<AGG>;
     L.fix = k_fixup<AGG>;
     L.inst_bytes = tag ? smem_for<AGG, true>(K, qcap, scap) : smem_for<AGG, false>(K, qcap, scap);
@@ -430,29 +457,41 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
 
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return fail(RS_ERR_CUDA, "cudaGetDevice failed");
+    const bool seq = (p->cfg.flags & RS_FLAG_SEQUENTIAL) != 0;
     if (p->device != dev || p->grid == 0) {
-        // Pick warps-per-CTA (instances per CTA) to pack the most instances per SM.
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        int best = 0, best_w = 1;
-        for (int w = WPB; w >= 1; w >>= 1) {
-            const uint32_t bytes = L.inst_bytes * w;
-            if (cudaFuncSetAttribute(L.main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
-                cudaGetLastError();
-                continue;
+        if (seq) {
+            // sequential scheduler: one instance per warp; pick warps-per-CTA to
+            // pack the most instances per SM
+            int best = 0, best_w = 1;
+            for (int w = WPB; w >= 1; w >>= 1) {
+                const uint32_t bytes = L.inst_bytes * w;
+                if (cudaFuncSetAttribute(L.main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
+                    cudaGetLastError();
+                    continue;
+                }
+                int per_sm = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.main, w * 32, bytes);
+                if (per_sm * w > best) { best = per_sm * w; best_w = w; }
             }
+            if (best < 1) return fail(RS_ERR_UNSUPPORTED, "pipeline does not fit on an SM (queue/signal capacities too large)");
+            p->wpb = best_w;
+            p->grid = p->cfg.grid > 0 ? p->cfg.grid : sms * (best / best_w);
+        } else {
+            // warp-specialised: one instance per CTA, one warp per node
+            p->wpb = p->nst + 2;
+            if (cudaFuncSetAttribute(L.ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.ws_bytes) != cudaSuccess)
+                return fail(RS_ERR_UNSUPPORTED, "pipeline shared memory exceeds the per-CTA limit");
             int per_sm = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.main, w * 32, bytes);
-            if (per_sm * w > best) { best = per_sm * w; best_w = w; }
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.ws, p->wpb * 32, L.ws_bytes);
+            if (per_sm < 1) return fail(RS_ERR_UNSUPPORTED, "pipeline does not fit on an SM (queue/signal capacities too large)");
+            p->grid = p->cfg.grid > 0 ? p->cfg.grid : sms * per_sm;
         }
-        if (best < 1) return fail(RS_ERR_UNSUPPORTED, "pipeline does not fit on an SM (queue/signal capacities too large)");
-        p->wpb = best_w;
-        const int blocks = best / best_w;
-        p->grid = p->cfg.grid > 0 ? p->cfg.grid : sms * blocks;
         p->device = dev;
     }
-    const uint32_t cta_smem = L.inst_bytes * p->wpb;
-    cudaFuncSetAttribute(L.main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cta_smem);
+    const uint32_t cta_smem = seq ? L.inst_bytes * p->wpb : L.ws_bytes;
+    cudaFuncSetAttribute(seq ? L.main : L.ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cta_smem);
 
     KParams K;
     std::memset(&K, 0, sizeof K);
@@ -486,7 +525,8 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
     if (timing) cudaEventRecord(p->ev[0], stream);
     L.pre<<<pre_blocks, 256, 0, stream>>>(K, 4 * (p->nst + 2));
     if (timing) cudaEventRecord(p->ev[1], stream);
-    L.main<<<p->grid, p->wpb * 32, cta_smem, stream>>>(K);
+    if (seq) L.main<<<p->grid, p->wpb * 32, cta_smem, stream>>>(K);
+    else L.ws<<<p->grid, p->wpb * 32, cta_smem, stream>>>(K);
     if (timing) cudaEventRecord(p->ev[2], stream);
     int fix_blocks = (int)std::min<long long>((wl.max_chunks + 255) / 256, 148 * 8);
     L.fix<<<std::max(fix_blocks, 1), 256, 0, stream>>>(K);

@@ -65,6 +65,24 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
     return ok != 0;
 }
 
+// Warp-uniform probe: lane 0 tests the phase, the verdict is broadcast and
+// __syncwarp carries lane 0's acquire to the other lanes.  (Per-lane probes
+// can disagree when the phase completes while the instruction executes.)
+__device__ __forceinline__ bool mbar_test_uniform(uint64_t *bar, uint32_t parity) {
+    bool ok = false;
+    if ((threadIdx.x & 31u) == 0) ok = mbar_test(bar, parity);
+    ok = __shfl_sync(kFull, (int)ok, 0) != 0;
+    __syncwarp();
+    return ok;
+}
+__device__ __forceinline__ bool mbar_try_wait_uniform(uint64_t *bar, uint32_t parity) {
+    bool ok = false;
+    if ((threadIdx.x & 31u) == 0) ok = mbar_try_wait(bar, parity);
+    ok = __shfl_sync(kFull, (int)ok, 0) != 0;
+    __syncwarp();
+    return ok;
+}
+
 // ------------------------------------------------------------- TMA (bulk)
 // 1-D bulk copy global -> shared, completion signalled on `bar` as tx bytes.
 // dst/src 16-byte aligned, bytes a multiple of 16.

@@ -37,6 +37,79 @@ struct OpAffine {
     }
 };
 
+// Full ensembles of a FILTER/TRANSFORM node, specialised per op and shared
+// by every stage node (one copy of the code keeps the hot loop inside the
+// instruction cache).  Item t of an ensemble lives in lane t%32, slot t/32.
+// NS slices (NS*32 items, one or two ensembles) are processed together: all
+// loads first, then the predicates, then the stable ballot/popc compaction
+// into the output queue (push) -- NS-way instruction-level parallelism.
+template <bool TAG, int NS, class Op>
+__device__ __forceinline__ void filter_slices(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
+                                              uint32_t *out, uint32_t *tout, uint32_t qmask, uint32_t &tl,
+                                              const Op &op, uint32_t lt) {
+    const uint32_t lane = threadIdx.x & 31u;
+    uint32_t v[NS], tg[NS];
+    bool keep[NS];
+    if (((h & imask) + NS * 32) <= imask + 1) {        // input range does not wrap the ring
+        const uint32_t *src = in + (h & imask) + lane;
+#pragma unroll
+        for (int j = 0; j < NS; ++j) v[j] = src[32 * j];
+        if constexpr (TAG) {
+            const uint32_t *ts = tin + (h & imask) + lane;
+#pragma unroll
+            for (int j = 0; j < NS; ++j) tg[j] = ts[32 * j];
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < NS; ++j) v[j] = in[(h + 32 * j + lane) & imask];
+        if constexpr (TAG) {
+#pragma unroll
+            for (int j = 0; j < NS; ++j) tg[j] = tin[(h + 32 * j + lane) & imask];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NS; ++j) keep[j] = op(v[j]);
+    uint32_t mk[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) mk[j] = __ballot_sync(kFull, keep[j]);
+    if (((tl & qmask) + NS * 32) <= qmask + 1) {        // output range does not wrap the ring
+        uint32_t *dst = out + (tl & qmask);
+        uint32_t *tdst = TAG ? tout + (tl & qmask) : nullptr;
+        uint32_t off = 0;
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+            if (keep[j]) {
+                const uint32_t o = off + __popc(mk[j] & lt);
+                dst[o] = v[j];
+                if constexpr (TAG) tdst[o] = tg[j];
+            }
+            off += __popc(mk[j]);
+        }
+        tl += off;
+    } else {
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+            if (keep[j]) {
+                const uint32_t pos = (tl + __popc(mk[j] & lt)) & qmask;
+                out[pos] = v[j];
+                if constexpr (TAG) tout[pos] = tg[j];
+            }
+            tl += __popc(mk[j]);
+        }
+    }
+}
+
+template <bool TAG, class Op>
+__device__ __noinline__ uint32_t filter_batch(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
+                                              uint32_t nens, uint32_t *out, uint32_t *tout, uint32_t qmask,
+                                              uint32_t tl, const Op op, uint32_t lt) {
+    uint32_t k = 0;
+    for (; k + 2 <= nens; k += 2, h += 2 * W) filter_slices<TAG, 2 * IPL>(in, tin, imask, h, out, tout, qmask, tl, op, lt);
+    if (k < nens) filter_slices<TAG, IPL>(in, tin, imask, h, out, tout, qmask, tl, op, lt);
+    __syncwarp();
+    return tl;
+}
+
 struct Chunk {
     int32_t k;             // chunk id (-1 = empty slot)
     long long beg, end;    // element range [beg, end)
@@ -415,7 +488,7 @@ struct Pipe {
 
     // ---------------------------------------------------------- stages
     __device__ __forceinline__ uint32_t landed_pos() {
-        while (landed_j < stg_j && mbar_test(&bar[landed_j % NST], (landed_j / NST) & 1u)) landed_j++;
+        while (landed_j < stg_j && mbar_test_uniform(&bar[landed_j % NST], (landed_j / NST) & 1u)) landed_j++;
         return landed_j * (uint32_t)SBLK;
     }
 
@@ -432,87 +505,34 @@ struct Pipe {
         return min(ql, E<e>().cur);
     }
 
-    // Full ensembles of a FILTER/TRANSFORM node, specialised per op.  Item t
-    // of an ensemble lives in lane t%32, slot t/32; loads are issued first
-    // (4-way ILP), then the predicates, then the stable ballot/popc
-    // compaction into the output queue (push).
     template <int n, class Op>
     __device__ __forceinline__ void filter_full(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                                 uint32_t nens, const Op op) {
-        uint32_t *out = Q<n>();
-        uint32_t *tout = T<n>();
-        uint32_t tl = E<n>().qt;
-        for (uint32_t k = 0; k < nens; ++k, h += W) {
-            uint32_t v[IPL], tg[IPL];
-            bool keep[IPL];
-            if (((h & imask) + W) <= imask + 1) {          // ensemble does not wrap the ring
-                const uint32_t *src = in + (h & imask) + lane;
-#pragma unroll
-                for (int j = 0; j < IPL; ++j) v[j] = src[32 * j];
-                if constexpr (TAG) {
-                    const uint32_t *ts = tin + (h & imask) + lane;
-#pragma unroll
-                    for (int j = 0; j < IPL; ++j) tg[j] = ts[32 * j];
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < IPL; ++j) v[j] = in[(h + 32 * j + lane) & imask];
-                if constexpr (TAG) {
-#pragma unroll
-                    for (int j = 0; j < IPL; ++j) tg[j] = tin[(h + 32 * j + lane) & imask];
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < IPL; ++j) keep[j] = op(v[j]);
-            uint32_t mk[IPL];
-#pragma unroll
-            for (int j = 0; j < IPL; ++j) mk[j] = __ballot_sync(kFull, keep[j]);
-            if (((tl & qmask) + W) <= qcap) {              // output does not wrap the ring
-                uint32_t *dst = out + (tl & qmask);
-                uint32_t *tdst = TAG ? tout + (tl & qmask) : nullptr;
-                uint32_t off = 0;
-#pragma unroll
-                for (int j = 0; j < IPL; ++j) {
-                    if (keep[j]) {
-                        const uint32_t o = off + __popc(mk[j] & lt);
-                        dst[o] = v[j];
-                        if constexpr (TAG) tdst[o] = tg[j];
-                    }
-                    off += __popc(mk[j]);
-                }
-                tl += off;
-            } else {
-#pragma unroll
-                for (int j = 0; j < IPL; ++j) {
-                    if (keep[j]) {
-                        const uint32_t pos = (tl + __popc(mk[j] & lt)) & qmask;
-                        out[pos] = v[j];
-                        if constexpr (TAG) tout[pos] = tg[j];
-                    }
-                    tl += __popc(mk[j]);
-                }
-            }
-        }
+        const uint32_t tl = filter_batch<TAG, Op>(in, tin, imask, h, nens, Q<n>(), T<n>(), qmask, E<n>().qt, op, lt);
         E<n>().sent += tl - E<n>().qt;
         E<n>().qt = tl;
     }
 
-    // Full ensembles of the aggregate (signal strategy: one region per
-    // ensemble, P:495-499 -> plain per-lane accumulation, a::run P:533).
-    __device__ __forceinline__ void agg_full(const uint32_t *in, uint32_t imask, uint32_t h, uint32_t nens) {
-        for (uint32_t k = 0; k < nens; ++k, h += W) {
-            uint32_t v[IPL];
-            if (((h & imask) + W) <= imask + 1) {
-                const uint32_t *src = in + (h & imask) + lane;
+    template <int NS>
+    __device__ __forceinline__ void agg_slices(const uint32_t *in, uint32_t imask, uint32_t h) {
+        uint32_t v[NS];
+        if (((h & imask) + NS * 32) <= imask + 1) {
+            const uint32_t *src = in + (h & imask) + lane;
 #pragma unroll
-                for (int j = 0; j < IPL; ++j) v[j] = src[32 * j];
-            } else {
+            for (int j = 0; j < NS; ++j) v[j] = src[32 * j];
+        } else {
 #pragma unroll
-                for (int j = 0; j < IPL; ++j) v[j] = in[(h + 32 * j + lane) & imask];
-            }
-#pragma unroll
-            for (int j = 0; j < IPL; ++j) acc = AT::comb(acc, AT::lift(v[j]));
+            for (int j = 0; j < NS; ++j) v[j] = in[(h + 32 * j + lane) & imask];
         }
+        A part = AT::lift(v[0]);
+#pragma unroll
+        for (int j = 1; j < NS; ++j) part = AT::comb(part, AT::lift(v[j]));
+        acc = AT::comb(acc, part);
+    }
+    __device__ __forceinline__ void agg_full(const uint32_t *in, uint32_t imask, uint32_t h, uint32_t nens) {
+        uint32_t k = 0;
+        for (; k + 2 <= nens; k += 2, h += 2 * W) agg_slices<2 * IPL>(in, imask, h);
+        if (k < nens) agg_slices<IPL>(in, imask, h);
     }
 
     template <int n>
@@ -767,7 +787,7 @@ struct Pipe {
             // nothing fireable: wait for the oldest in-flight TMA stage
             if (landed_j < stg_j) {
                 uint32_t spins = 0;
-                while (!mbar_try_wait(&bar[landed_j % NST], (landed_j / NST) & 1u)) {
+                while (!mbar_try_wait_uniform(&bar[landed_j % NST], (landed_j / NST) & 1u)) {
                     if (++spins > (1u << 24)) break;
                 }
                 if (spins > (1u << 24)) {
@@ -784,7 +804,7 @@ struct Pipe {
         if constexpr (TAG) flush_tagged();
         // drain outstanding TMA stages before the CTA's shared memory is released
         for (uint32_t spins = 0; landed_j < stg_j && spins < (1u << 26); ++spins) {
-            if (mbar_try_wait(&bar[landed_j % NST], (landed_j / NST) & 1u)) landed_j++;
+            if (mbar_try_wait_uniform(&bar[landed_j % NST], (landed_j / NST) & 1u)) landed_j++;
         }
         if (P.flags & RS_FLAG_STATS) flush_stats<0>();
     }

@@ -30,8 +30,9 @@ def rs():
     return rs
 
 
-def run_gpu(rs, vals, off, stages, agg, strategy="signal", elems_pad=0, **cfg):
-    p = rs.Pipeline(stages, agg, strategy=strategy, **cfg)
+def run_gpu(rs, vals, off, stages, agg, strategy="signal", mode="ws", **cfg):
+    flags = rs.RS_FLAG_STATS | (rs.RS_FLAG_SEQUENTIAL if mode == "seq" else 0)
+    p = rs.Pipeline(stages, agg, strategy=strategy, flags=flags, **cfg)
     dev = torch.device("cuda:0")
     e = torch.from_numpy(np.ascontiguousarray(vals)).to(dev)
     o = torch.from_numpy(np.ascontiguousarray(off)).to(dev)
@@ -112,21 +113,23 @@ def _case(seed, agg, R=None, dist=None, L=None, base=None):
 
 @pytest.mark.parametrize("seed", range(24))
 @pytest.mark.parametrize("strategy", ["signal", "tagged"])
-def test_random_parity(rs, seed, strategy):
+@pytest.mark.parametrize("mode", ["ws", "seq"])
+def test_random_parity(rs, seed, strategy, mode):
     agg = ["sum_i64", "sum_f32", "count_min_u32"][seed % 3]
     vals, off, stages = _case(seed, agg)
     rnd = random.Random(seed * 7 + 1)
     cfg = dict(chunk=rnd.choice([2048, 4096, 8192]), grid=rnd.choice([0, 0, 1, 3]),
                queue_cap=rnd.choice([256, 512]), signal_cap=rnd.choice([4, 16, 128]))
     ref = oracle.brute(vals, off, stages, agg)
-    got, st, _ = run_gpu(rs, vals, off, stages, agg, strategy, **cfg)
+    got, st, _ = run_gpu(rs, vals, off, stages, agg, strategy, mode, **cfg)
     assert_parity(got, ref, agg)
     assert st[0][2] == off[-1] - off[0]
 
 
 @pytest.mark.parametrize("strategy", ["signal", "tagged"])
 @pytest.mark.parametrize("L", [1, 4, 32, 127, 128, 129, 256, 4096, 100000])
-def test_region_lengths(rs, strategy, L):
+@pytest.mark.parametrize("mode", ["ws", "seq"])
+def test_region_lengths(rs, strategy, L, mode):
     """Region lengths 1..4096 (north star) plus regions far longer than a chunk."""
     N = 1 << 18
     R = max(1, N // L)
@@ -136,7 +139,7 @@ def test_region_lengths(rs, strategy, L):
         vals = synth.values(int(off[-1]), "i32", seed=L + 5)
         stages = synth.sweep_stages(3)
         ref = oracle.brute(vals, off, stages, "sum_i64")
-        got, st, _ = run_gpu(rs, vals, off, stages, "sum_i64", strategy)
+        got, st, _ = run_gpu(rs, vals, off, stages, "sum_i64", strategy, mode)
         assert_parity(got, ref, "sum_i64")
 
 
@@ -193,14 +196,17 @@ def test_grid_and_capacity_invariance(rs):
     vals = synth.values(int(off[-1]), "i32", 12)
     stages = synth.sweep_stages(3)
     ref = oracle.brute(vals, off, stages, "sum_i64")
-    for cfg in (dict(grid=1), dict(grid=2, chunk=2048), dict(queue_cap=1024, signal_cap=8), dict(signal_cap=4)):
+    for cfg in (dict(grid=1), dict(grid=2, chunk=2048), dict(queue_cap=1024, signal_cap=8), dict(signal_cap=4),
+                dict(queue_cap=256)):
         for strat in ("signal", "tagged"):
-            got, _, _ = run_gpu(rs, vals, off, stages, "sum_i64", strat, **cfg)
-            assert_parity(got, ref, "sum_i64")
+            for mode in ("ws", "seq"):
+                got, _, _ = run_gpu(rs, vals, off, stages, "sum_i64", strat, mode, **cfg)
+                assert_parity(got, ref, "sum_i64")
 
 
 @pytest.mark.parametrize("R", [32, 64, 96, 128, 256, 512, 1024])
-def test_occupancy_closed_form_gpu(rs, R):
+@pytest.mark.parametrize("mode", ["ws", "seq"])
+def test_occupancy_closed_form_gpu(rs, R, mode):
     """One instance (grid=1), fixed regions dividing the chunk, pass-all
     stages, full-first: the aggregate's lane fraction equals R/(w ceil(R/w))
     exactly, as the oracle's interpreter gives."""
@@ -209,7 +215,7 @@ def test_occupancy_closed_form_gpu(rs, R):
     vals = synth.values(int(off[-1]), "i32", R)
     stages = [("hash_lt", 0x9E3779B1, 256)] * 2
     chunk = 1 << max(11, int(off[-1] - 1).bit_length())     # one chunk: no region is split
-    got, st, _ = run_gpu(rs, vals, off, stages, "sum_i64", "signal", grid=1, chunk=chunk)
+    got, st, _ = run_gpu(rs, vals, off, stages, "sum_i64", "signal", mode, grid=1, chunk=chunk)
     ref = oracle.interp(vals, off, stages, "sum_i64", w=128, qcap=1024, scap=256)
     np.testing.assert_array_equal(got[0], ref["out"][0])
     num, den = R, 128 * math.ceil(R / 128)
