@@ -334,11 +334,10 @@ def run_ours(args):
     # ---- CPU oracle baseline (rank 0, N = 1 only), bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        n_s = min(n, 1 << 24)
-        r_s = int(torch.searchsorted(off, off[0] + n_s).item())
-        vh = vals[: int(off[r_s].item())].cpu().numpy()
-        oh = off[: r_s + 1].cpu().numpy()
-        rate, cores, desc = oracle_rate(vh, oh, spec["stages"], spec["agg"], budget_s=10.0)
+        # the whole workload fits the ~10-30 s CPU budget of the oracle's interpreter
+        vh = vals.cpu().numpy()
+        oh = off.cpu().numpy()
+        rate, cores, desc = oracle_rate(vh, oh, spec["stages"], spec["agg"], budget_s=20.0)
         cpu = {"value": rate, "unit": "items/s", "cores": cores, "kind": "oracle", "sample": desc}
 
     sweep = None
@@ -395,7 +394,7 @@ def run_sweep(rs, torch, dev, args):
                 p = rs.Pipeline(synth.sweep_stages(3), "sum_i64", strategy=strat,
                                 flags=rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING)
                 out = p.alloc_outputs(R, dev)
-                ws = p.alloc_workspace(R, n, dev)
+                ws = p.alloc_workspace(R, vals.numel(), dev)
                 p.run(vals, off, out, ws)
                 torch.cuda.synchronize()
                 ms = []
@@ -423,9 +422,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="sweep_fixed_L4096")
     ap.add_argument("--strategy", default="signal", choices=["signal", "tagged"])
-    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--no-sweep", dest="sweep", action="store_false")
     ap.add_argument("--sweep-L", default="1,4,32,256,4096")
-    ap.add_argument("--sweep-reps", type=int, default=3)
+    ap.add_argument("--sweep-reps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -97,15 +97,16 @@ enum {
     RS_FLAG_STATS = 1u,      /* collect per-node occupancy counters (default on)     */
     RS_FLAG_VALIDATE = 2u,   /* device-check offsets monotone and <= n_elems          */
     RS_FLAG_TIMING = 4u,     /* record CUDA events around each kernel of a run        */
-    RS_FLAG_SEQUENTIAL = 8u  /* one warp per instance firing one node at a time (the
-                                paper's per-processor scheduler) instead of
-                                the default warp-specialised instance (one warp per node) */
+    RS_FLAG_WARP_SPECIALIZED = 8u  /* one CTA per instance with one warp per node, nodes
+                                      running concurrently (signals carry emission positions),
+                                      instead of the default one-warp instance whose scheduler
+                                      fires one node at a time */
 };
 
 typedef struct {
     int32_t strategy;        /* rs_strategy                                          */
     uint32_t simd_width;     /* ensemble capacity w in items; only 128 is built */
-    uint32_t queue_cap;      /* inter-stage data queue capacity (items, power of 2, >= 2w; default 8w) */
+    uint32_t queue_cap;      /* inter-stage data queue capacity (items, power of 2, >= 2w; default 16w) */
     uint32_t signal_cap;     /* signal queue capacity (entries, power of 2, >= 4)    */
     int32_t grid;            /* persistent CTAs; 0 = fill the device                  */
     uint32_t chunk;          /* children per parent-stream claim; 0 = default        */

@@ -336,7 +336,7 @@ rs_status rs_config_default(rs_config *cfg) {
     if (!cfg) return fail(RS_ERR_INVALID_ARG, "cfg is NULL");
     cfg->strategy = RS_STRATEGY_SIGNAL;
     cfg->simd_width = W;
-    cfg->queue_cap = 8 * W;    // SPEC default 8w
+    cfg->queue_cap = 16 * W;   // 2048 items (SPEC's 8w default doubled: amortises firings)
     cfg->signal_cap = 128;
     cfg->grid = 0;
     cfg->chunk = 0;
@@ -374,7 +374,7 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
         return fail(RS_ERR_INVALID_ARG, "bad strategy");
     if (cfg.simd_width == 0) cfg.simd_width = W;
     if (cfg.simd_width != (uint32_t)W) return fail(RS_ERR_UNSUPPORTED, "only simd_width 128 is built");
-    if (cfg.queue_cap == 0) cfg.queue_cap = 8 * W;
+    if (cfg.queue_cap == 0) cfg.queue_cap = 16 * W;
     if (cfg.signal_cap == 0) cfg.signal_cap = 128;
     if (!is_pow2(cfg.queue_cap) || cfg.queue_cap < 2 * W || cfg.queue_cap > 65536)
         return fail(RS_ERR_UNSUPPORTED, "queue_cap must be a power of 2 in [256, 65536]");
@@ -457,7 +457,7 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
 
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return fail(RS_ERR_CUDA, "cudaGetDevice failed");
-    const bool seq = (p->cfg.flags & RS_FLAG_SEQUENTIAL) != 0;
+    const bool seq = (p->cfg.flags & RS_FLAG_WARP_SPECIALIZED) == 0;
     if (p->device != dev || p->grid == 0) {
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -1,4 +1,4 @@
-// rs_ws.cuh — warp-specialised pipeline instance (default execution mode).
+// rs_ws.cuh — warp-specialised pipeline instance (RS_FLAG_WARP_SPECIALIZED).
 //
 // One CTA = one pipeline instance; warp n runs node n continuously:
 //   warp 0      ENUMERATE  (TMA staging of the element stream + Begin/End
@@ -47,6 +47,7 @@ struct WS {
     static constexpr int SBLK = TAG ? 256 : 512;     // elements per TMA stage
     static constexpr int RING0 = NST * SBLK;         // Q0 ring capacity (items)
     static constexpr int NW = K + 2;                 // warps per instance
+    static constexpr int BMIN = 4;                   // preferred minimum ensembles per firing
 
     __host__ __device__ static constexpr uint32_t off_bar() { return 256; }
     __host__ __device__ static constexpr uint32_t off_q0() { return 384; }
@@ -91,12 +92,11 @@ struct WS {
 
     // Make this warp's shared-memory writes (queue items, tags, signal
     // entries -- written by any lane) visible before the position word that
-    // announces them: every lane fences, the warp synchronises, lane 0
-    // releases the new position.  Consumers read position words with
+    // announces them: the warp synchronises (memory-ordering among its lanes),
+    // lane 0 releases the new position.  Consumers read position words with
     // ld.acquire before touching the items.
     __device__ __forceinline__ void publish(uint32_t *w, uint32_t v) const {
-        __threadfence_block();
-        __syncwarp();
+        __syncwarp();            // orders every lane's prior shared writes before lane 0's release
         if (lane == 0) st_rel(w, v);
     }
 
@@ -497,6 +497,7 @@ struct WS {
         const uint32_t *in = Q(ei), *tin = T(ei);
         const uint32_t im = imask(ei);
         uint32_t otail = 0, ost = 0;           // own output positions
+        uint32_t wait_small = 0;
         uint32_t ohead = 0, osh = 0;           // consumer positions last seen
         uint32_t backoff = 0, idle = 0;
         I.head = ctl(ei)->head;                // Q0 may start at the chunk-0 pad (set before the CTA barrier)
@@ -516,7 +517,17 @@ struct WS {
                     space = qcap - (otail - ohead);
                 }
                 const uint32_t e = min(avail, space);
-                if (e >= (uint32_t)W) {
+                // Batch at least BMIN ensembles per firing so the scheduling cost is
+                // amortised; smaller batches only when the limit is a signal stamp,
+                // the output queue, or the drained input.
+                bool go = e >= (uint32_t)W;
+                if (go && e < (uint32_t)(BMIN * W) && !(spend && lim == stamp) && space >= avail && !I.done &&
+                    wait_small < 8) {
+                    go = false;
+                    ++wait_small;
+                }
+                if (go) {
+                    wait_small = 0;
                     const uint32_t nens = e / W;
                     const uint32_t t2 = filter_batch<TAG, Op>(in, tin, im, I.head, nens, out, tout, qmask, otail, op, lt);
                     I.head += nens * W;
@@ -665,7 +676,7 @@ struct WS {
         G.akey = 0xffffffffu;
         const uint32_t *in = Q(ei), *tin = T(ei);
         const uint32_t im = imask(ei);
-        uint32_t backoff = 0, idle = 0;
+        uint32_t backoff = 0, idle = 0, wait_small = 0;
         I.head = ctl(ei)->head;
         I.tail = I.head;
         for (;;) {
@@ -677,7 +688,13 @@ struct WS {
                 const uint32_t lim = limit(I, ei, spend, stamp, kind, key);
                 if ((int)(lim - I.head) < 0) { debug_fail(n, I, lim, spend, stamp, key, kind); return; }
                 const uint32_t avail = lim - I.head;
-                if (avail >= (uint32_t)W) {
+                bool go = avail >= (uint32_t)W;
+                if (go && avail < (uint32_t)(BMIN * W) && !(spend && lim == stamp) && !I.done && wait_small < 8) {
+                    go = false;
+                    ++wait_small;
+                }
+                if (go) {
+                    wait_small = 0;
                     const uint32_t nens = avail / W;
                     uint32_t h = I.head;
                     if constexpr (!TAG) {

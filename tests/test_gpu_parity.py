@@ -31,7 +31,7 @@ def rs():
 
 
 def run_gpu(rs, vals, off, stages, agg, strategy="signal", mode="ws", **cfg):
-    flags = rs.RS_FLAG_STATS | (rs.RS_FLAG_SEQUENTIAL if mode == "seq" else 0)
+    flags = rs.RS_FLAG_STATS | (rs.RS_FLAG_WARP_SPECIALIZED if mode == "ws" else 0)
     p = rs.Pipeline(stages, agg, strategy=strategy, flags=flags, **cfg)
     dev = torch.device("cuda:0")
     e = torch.from_numpy(np.ascontiguousarray(vals)).to(dev)

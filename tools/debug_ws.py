@@ -6,7 +6,7 @@ import oracle, synth
 import paper_2006_07478_b200 as rs
 
 def run(vals, off, stages, strategy, mode, **cfg):
-    flags = rs.RS_FLAG_STATS | (rs.RS_FLAG_SEQUENTIAL if mode == "seq" else 0)
+    flags = rs.RS_FLAG_STATS | (rs.RS_FLAG_WARP_SPECIALIZED if mode == "ws" else 0)
     p = rs.Pipeline(stages, "sum_i64", strategy=strategy, flags=flags, **cfg)
     e = torch.from_numpy(vals).cuda(); o = torch.from_numpy(off).cuda()
     out = p.alloc_outputs(off.size - 1); ws = p.alloc_workspace(off.size - 1, vals.size)

@@ -15,15 +15,16 @@ ap.add_argument("--qcap", type=int, default=0)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--matrix", action="store_true")
 ap.add_argument("--qmatrix", action="store_true")
+ap.add_argument("--kmatrix", action="store_true")
 ap.add_argument("--scap", type=int, default=0)
 a = ap.parse_args()
 
 vals = synth.torch_values(a.N, "i32", seed=1)
-def one(L, K, strategy, chunk, grid, qcap, reps, scap=0):
+def one(L, K, strategy, chunk, grid, qcap, reps, scap=0, seq=False):
     lens = torch.full((a.N // L,), L, dtype=torch.int64, device="cuda")
     off = synth.torch_offsets(lens)
     p = rs.Pipeline(synth.sweep_stages(K), "sum_i64", strategy=strategy, chunk=chunk, grid=grid,
-                    queue_cap=qcap, signal_cap=scap, flags=rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING)
+                    queue_cap=qcap, signal_cap=scap, flags=rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING | (0 if seq else rs.RS_FLAG_WARP_SPECIALIZED))
     R = off.numel() - 1
     out = p.alloc_outputs(R); ws = p.alloc_workspace(R, a.N)
     ms = []
@@ -33,7 +34,7 @@ def one(L, K, strategy, chunk, grid, qcap, reps, scap=0):
         if i: ms.append(t[1])
     m = statistics.median(ms)
     gbs = (4 * a.N + 16 * R) / (m / 1e3) / 1e9
-    print(f"L={L} K={K} {strategy} q={qcap} s={scap} chunk={chunk} grid={grid} geom={p.geometry()} main={m:.3f} ms  {a.N/(m/1e3)/1e9:.1f} Gitems/s  {gbs:.0f} GB/s  err={p.check()}", flush=True)
+    print(f"L={L} K={K} {strategy} {'seq' if seq else 'ws'} q={qcap} s={scap} chunk={chunk} grid={grid} geom={p.geometry()} main={m:.3f} ms  {a.N/(m/1e3)/1e9:.1f} Gitems/s  {gbs:.0f} GB/s  err={p.check()}", flush=True)
 
 # reference: plain bandwidth of a torch reduction over the same array
 x = vals
@@ -50,6 +51,10 @@ if a.matrix:
     for L in (32, 256):
         for st in ("signal", "tagged"):
             one(L, 3, st, a.chunk, a.grid, a.qcap, a.reps)
+elif a.kmatrix:
+    for seq in (False, True):
+        for K in (0, 1, 2, 3):
+            one(a.L, K, "signal", a.chunk, a.grid, 2048, a.reps, 0, seq)
 elif a.qmatrix:
     for st in ("signal", "tagged"):
         for q in (512, 1024, 2048):
