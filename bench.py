@@ -57,6 +57,7 @@ class Clocks:
         self.gpu = gpu_index
 
     def __enter__(self):
+        self.t_on = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu),
@@ -73,7 +74,16 @@ class Clocks:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.samples.append([x.strip() for x in line.split(",")])
+            self.samples.append([time.time()] + [x.strip() for x in line.split(",")])
+
+    def wait_ready(self, timeout=5.0):
+        """Block until the sampler delivers its first sample (nvidia-smi start-up)."""
+        t0 = time.time()
+        while self.proc and not self.samples and time.time() - t0 < timeout:
+            time.sleep(0.05)
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
 
     def __exit__(self, *a):
         if self.proc:
@@ -84,18 +94,25 @@ class Clocks:
                 self.proc.kill()
 
     def summary(self):
-        if not self.samples:
+        # samples inside the timed window (100 ms sampling; short windows take the
+        # nearest samples within +-0.25 s)
+        win = getattr(self, "window", None)
+        smp = self.samples
+        if win:
+            inside = [s for s in smp if win[0] <= s[0] <= win[1]]
+            smp = inside or [s for s in smp if win[0] - 0.25 <= s[0] <= win[1] + 0.25]
+        if not smp:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        sm = [float(s[1]) for s in smp if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in smp if s[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for s in self.samples:
-            for n, v in zip(names, s[3:7]):
+        for s in smp:
+            for n, v in zip(names, s[4:8]):
                 if v.strip().lower() == "active":
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons)}
+                "reasons": sorted(reasons), "samples": len(smp)}
 
 
 # ------------------------------------------------------------------ workloads
@@ -278,7 +295,9 @@ def run_ours(args):
     t1 = torch.cuda.Event(enable_timing=True)
     main_ms = []
     with Clocks(local) as clk:
+        clk.wait_ready()
         torch.cuda.synchronize()
+        w0 = time.time()
         t0.record(stream)
         for _ in range(args.steps):
             p.run(vals, off, out, ws)
@@ -286,6 +305,8 @@ def run_ours(args):
                 dist.gather(out[0], gather_buf if rank == 0 else None, dst=0)
         t1.record(stream)
         torch.cuda.synchronize()
+        clk.mark(w0, time.time())
+        time.sleep(0.3)
     total_ms = t0.elapsed_time(t1)
     # per-launch main-kernel time, measured live with events on the launching stream
     for _ in range(max(3, min(args.steps, 10))):

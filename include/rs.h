@@ -97,6 +97,7 @@ enum {
     RS_FLAG_STATS = 1u,      /* collect per-node occupancy counters (default on)     */
     RS_FLAG_VALIDATE = 2u,   /* device-check offsets monotone and <= n_elems          */
     RS_FLAG_TIMING = 4u,     /* record CUDA events around each kernel of a run        */
+    RS_FLAG_PROFILE = 16u,   /* per-node clock64() cycle counters (rs_pipeline_profile)  */
     RS_FLAG_WARP_SPECIALIZED = 8u  /* one CTA per instance with one warp per node, nodes
                                       running concurrently (signals carry emission positions),
                                       instead of the default one-warp instance whose scheduler
@@ -106,11 +107,13 @@ enum {
 typedef struct {
     int32_t strategy;        /* rs_strategy                                          */
     uint32_t simd_width;     /* ensemble capacity w in items; only 128 is built */
-    uint32_t queue_cap;      /* inter-stage data queue capacity (items, power of 2, >= 2w; default 16w) */
-    uint32_t signal_cap;     /* signal queue capacity (entries, power of 2, >= 4)    */
+    uint32_t queue_cap;      /* inter-stage data queue capacity (items, power of 2, >= 2w; 0 = auto: 8w with 2+ stages, else 16w) */
+    uint32_t signal_cap;     /* signal queue capacity (entries, power of 2, >= 4; 0 = auto) */
     int32_t grid;            /* persistent CTAs; 0 = fill the device                  */
     uint32_t chunk;          /* children per parent-stream claim; 0 = default        */
     uint32_t flags;          /* RS_FLAG_*                                            */
+    uint32_t q0_stage;       /* elements per TMA stage of the enumerate queue (4 stages);
+                                power of 2 in [128, 4096]; 0 = auto (256 tagged or 2+ stages, else 512) */
 } rs_config;
 
 /* Per-node occupancy counters (§2.2, §5).  Node 0 is the
@@ -171,6 +174,12 @@ rs_status rs_pipeline_run_host(rs_pipeline *p, const void *h_elems, int64_t n_el
 /* Copy the per-node counters of the last run into host_out[0..n_nodes-1]
  * (n_nodes = the create-time node count).  Synchronises `stream`. */
 rs_status rs_pipeline_stats(rs_pipeline *p, rs_node_stats *host_out, int n_nodes, rs_stream stream);
+
+/* Per-node cycle counters of the last run made with RS_FLAG_PROFILE (sequential
+ * mode; synchronises `stream`): host16[0] = enumerate, host16[1..K+1] = nodes,
+ * host16[K+2] = waiting on TMA, [8] = scheduler sweeps, [9] = waits,
+ * [10] = instances; cycles are summed over instances. */
+rs_status rs_pipeline_profile(rs_pipeline *p, uint64_t *host16, rs_stream stream);
 
 /* Read the device error word of the last run (synchronises `stream`).
  * Returns RS_ERR_PROTOCOL and sets *code (if non-NULL) when the device saw a

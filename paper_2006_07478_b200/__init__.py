@@ -23,10 +23,11 @@ OPS = {"none": 0, "hash_lt": 1, "lt_u32": 2, "class": 3, "scale_f32": 10, "affin
        "sum_i64": 20, "sum_f32": 21, "count_min_u32": 22, "count_xor64": 23}
 DTYPES = {"i32": 0, "u32": 1, "u8": 2, "f32": 3}
 STRATEGIES = {"signal": 0, "tagged": 1}
-RS_FLAG_STATS, RS_FLAG_VALIDATE, RS_FLAG_TIMING, RS_FLAG_WARP_SPECIALIZED = 1, 2, 4, 8
+RS_FLAG_STATS, RS_FLAG_VALIDATE, RS_FLAG_TIMING, RS_FLAG_WARP_SPECIALIZED, RS_FLAG_PROFILE = 1, 2, 4, 8, 16
 
 EXPORTS = ["rs_config_default", "rs_pipeline_create", "rs_pipeline_workspace_bytes", "rs_pipeline_run",
-           "rs_pipeline_run_host", "rs_pipeline_stats", "rs_pipeline_check", "rs_pipeline_kernel_times",
+           "rs_pipeline_run_host", "rs_pipeline_stats", "rs_pipeline_profile", "rs_pipeline_check",
+           "rs_pipeline_kernel_times",
            "rs_pipeline_launches",
            "rs_pipeline_geometry", "rs_pipeline_destroy", "rs_status_string", "rs_last_error"]
 
@@ -45,7 +46,7 @@ class rs_node(C.Structure):
 class rs_config(C.Structure):
     _fields_ = [("strategy", C.c_int32), ("simd_width", C.c_uint32), ("queue_cap", C.c_uint32),
                 ("signal_cap", C.c_uint32), ("grid", C.c_int32), ("chunk", C.c_uint32),
-                ("flags", C.c_uint32)]
+                ("flags", C.c_uint32), ("q0_stage", C.c_uint32)]
 
 
 class rs_node_stats(C.Structure):
@@ -75,6 +76,8 @@ def lib():
         L.rs_pipeline_run_host.argtypes = [vp, vp, i64, vp, i64, rs_aggregates, vp]
         L.rs_pipeline_stats.argtypes = [vp, vp, i32, vp]
         L.rs_pipeline_check.argtypes = [vp, vp, C.POINTER(C.c_int32)]
+        L.rs_pipeline_profile.argtypes = [vp, vp, vp]
+        L.rs_pipeline_profile.restype = i32
         L.rs_pipeline_kernel_times.argtypes = [vp, vp, vp]
         L.rs_pipeline_kernel_times.restype = i32
         L.rs_pipeline_launches.argtypes = [vp]
@@ -125,7 +128,7 @@ class Pipeline:
     ``agg``: aggregate op name.  Node list = [ENUMERATE] + stages + [AGGREGATE]."""
 
     def __init__(self, stages, agg, elem=None, strategy="signal", queue_cap=0, signal_cap=0, grid=0,
-                 chunk=0, flags=RS_FLAG_STATS, simd_width=128):
+                 chunk=0, flags=RS_FLAG_STATS, simd_width=128, q0_stage=0):
         L = lib()
         self.stages = list(stages)
         self.agg = agg
@@ -153,6 +156,7 @@ class Pipeline:
         cfg.grid = grid
         cfg.chunk = chunk
         cfg.flags = flags
+        cfg.q0_stage = q0_stage
         h = C.c_void_p()
         _check(L.rs_pipeline_create(nodes, len(self.stages) + 2, DTYPES[self.elem], C.byref(cfg), C.byref(h)))
         self.h = h
@@ -239,6 +243,14 @@ class Pipeline:
         code = C.c_int32(0)
         _check(lib().rs_pipeline_check(self.h, C.c_void_p(s), C.byref(code)))
         return code.value
+
+    def profile(self, stream=None):
+        """Per-node cycle counters of the last RS_FLAG_PROFILE run (see rs.h)."""
+        import torch
+        s = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        buf = (C.c_uint64 * 16)()
+        _check(lib().rs_pipeline_profile(self.h, buf, C.c_void_p(s)))
+        return list(buf)
 
     def kernel_times(self, stream=None):
         """(prepass, pipeline, fixup) device ms of the last run (RS_FLAG_TIMING)."""

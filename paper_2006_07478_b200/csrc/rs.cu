@@ -76,6 +76,7 @@ struct KParams {
     long long max_chunks;
     uint32_t C;                     // chunk length (children)
     uint32_t qcap, scap;            // queue / signal capacities (powers of 2)
+    uint32_t q0_stage;              // Q0 TMA stage size in elements (sequential kernel)
     uint32_t flags;
     int32_t tagged;
     int32_t nst;
@@ -249,13 +250,13 @@ uint32_t smem_ws(int K, uint32_t qcap, uint32_t scap) {
 }
 
 template <int AGG, bool TAG>
-uint32_t smem_for(int K, uint32_t qcap, uint32_t scap) {
+uint32_t smem_for(int K, uint32_t qcap, uint32_t scap, uint32_t sblk) {
     switch (K) {
-        case 0: return Pipe<0, AGG, TAG>::smem_bytes(qcap, scap);
-        case 1: return Pipe<1, AGG, TAG>::smem_bytes(qcap, scap);
-        case 2: return Pipe<2, AGG, TAG>::smem_bytes(qcap, scap);
-        case 3: return Pipe<3, AGG, TAG>::smem_bytes(qcap, scap);
-        default: return Pipe<4, AGG, TAG>::smem_bytes(qcap, scap);
+        case 0: return Pipe<0, AGG, TAG>::smem_bytes(qcap, scap, sblk);
+        case 1: return Pipe<1, AGG, TAG>::smem_bytes(qcap, scap, sblk);
+        case 2: return Pipe<2, AGG, TAG>::smem_bytes(qcap, scap, sblk);
+        case 3: return Pipe<3, AGG, TAG>::smem_bytes(qcap, scap, sblk);
+        default: return Pipe<4, AGG, TAG>::smem_bytes(qcap, scap, sblk);
     }
 }
 
@@ -270,14 +271,14 @@ struct Launch {
 };
 
 template <int AGG>
-Launch launch_for(int K, bool tag, uint32_t qcap, uint32_t scap) {
+Launch launch_for(int K, bool tag, uint32_t qcap, uint32_t scap, uint32_t sblk) {
     Launch L;
     L.main = tag ? pick_k<AGG, true>(K) : pick_k<AGG, false>(K);
     L.ws = tag ? pick_ws<AGG, true>(K) : pick_ws<AGG, false>(K);
     L.ws_bytes = tag ? smem_ws<AGG, true>(K, qcap, scap) : smem_ws<AGG, false>(K, qcap, scap);
     L.pre = k_prepass<AGG>;
     L.fix = k_fixup<AGG>;
-    L.inst_bytes = tag ? smem_for<AGG, true>(K, qcap, scap) : smem_for<AGG, false>(K, qcap, scap);
+    L.inst_bytes = tag ? smem_for<AGG, true>(K, qcap, scap, sblk) : smem_for<AGG, false>(K, qcap, scap, sblk);
     L.out_bytes0 = AggT<AGG>::bytes0;
     L.out_bytes1 = AggT<AGG>::bytes1;
     return L;
@@ -285,9 +286,9 @@ Launch launch_for(int K, bool tag, uint32_t qcap, uint32_t scap) {
 
 bool get_launch(const rs_pipeline *p, Launch *L) {
     switch (p->agg) {
-        case RS_OP_SUM_I64: *L = launch_for<20>(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap); return true;
-        case RS_OP_SUM_F32: *L = launch_for<21>(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap); return true;
-        case RS_OP_COUNT_MIN_U32: *L = launch_for<22>(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap); return true;
+        case RS_OP_SUM_I64: *L = launch_for<20>(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
+        case RS_OP_SUM_F32: *L = launch_for<21>(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
+        case RS_OP_COUNT_MIN_U32: *L = launch_for<22>(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
     }
     return false;
 }
@@ -305,7 +306,7 @@ WsLayout layout(const rs_pipeline *p, long long n_regions, long long n_elems, co
     w.max_chunks = (n_elems + 16) / C + 2;
     w.hdr = 0;
     w.stats = 256;
-    w.fr = w.stats + align256(sizeof(unsigned long long) * 4 * (MAXK + 2));
+    w.fr = w.stats + align256(sizeof(unsigned long long) * (4 * (MAXK + 2) + 16));
     w.part0 = w.fr + align256(sizeof(uint32_t) * (size_t)(w.max_chunks + 1));
     w.part1 = w.part0 + align256((size_t)L.out_bytes0 * 2 * (size_t)w.max_chunks);
     w.total = w.part1 + align256((size_t)(L.out_bytes1 ? L.out_bytes1 : 1) * 2 * (size_t)w.max_chunks);
@@ -336,11 +337,12 @@ rs_status rs_config_default(rs_config *cfg) {
     if (!cfg) return fail(RS_ERR_INVALID_ARG, "cfg is NULL");
     cfg->strategy = RS_STRATEGY_SIGNAL;
     cfg->simd_width = W;
-    cfg->queue_cap = 16 * W;   // 2048 items (SPEC's 8w default doubled: amortises firings)
-    cfg->signal_cap = 128;
+    cfg->queue_cap = 0;        // 0 = auto (rs_pipeline_create picks 8w or 16w by stage count)
+    cfg->signal_cap = 0;       // 0 = auto
     cfg->grid = 0;
     cfg->chunk = 0;
     cfg->flags = RS_FLAG_STATS;
+    cfg->q0_stage = 0;
     return RS_OK;
 }
 
@@ -374,8 +376,13 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
         return fail(RS_ERR_INVALID_ARG, "bad strategy");
     if (cfg.simd_width == 0) cfg.simd_width = W;
     if (cfg.simd_width != (uint32_t)W) return fail(RS_ERR_UNSUPPORTED, "only simd_width 128 is built");
-    if (cfg.queue_cap == 0) cfg.queue_cap = 16 * W;
-    if (cfg.signal_cap == 0) cfg.signal_cap = 128;
+    // Defaults tuned on B200 (profiles/r1_tuning.txt): deep queues amortise the
+    // scheduler for short pipelines; with 2+ stages a smaller footprint fits
+    // twice the instances per SM, which wins.
+    const int nst_ = n_nodes - 2;
+    if (cfg.queue_cap == 0) cfg.queue_cap = nst_ >= 2 ? 8 * W : 16 * W;
+    if (cfg.signal_cap == 0) cfg.signal_cap = nst_ >= 2 ? 64 : 128;
+    if (cfg.q0_stage == 0) cfg.q0_stage = (cfg.strategy == RS_STRATEGY_TAGGED || nst_ >= 2) ? 256 : 512;
     if (!is_pow2(cfg.queue_cap) || cfg.queue_cap < 2 * W || cfg.queue_cap > 65536)
         return fail(RS_ERR_UNSUPPORTED, "queue_cap must be a power of 2 in [256, 65536]");
     if (!is_pow2(cfg.signal_cap) || cfg.signal_cap < 4 || cfg.signal_cap > 65536)
@@ -384,6 +391,9 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     if (!is_pow2(cfg.chunk) || cfg.chunk < 2048 || cfg.chunk > (1u << 24))
         return fail(RS_ERR_UNSUPPORTED, "chunk must be a power of 2 in [2048, 2^24]");
     if (cfg.grid < 0) return fail(RS_ERR_INVALID_ARG, "grid must be >= 0");
+    if (!is_pow2(cfg.q0_stage) || cfg.q0_stage < 128 || cfg.q0_stage > 4096)
+        return fail(RS_ERR_UNSUPPORTED, "q0_stage must be a power of 2 in [128, 4096]");
+    if (cfg.chunk < NST * cfg.q0_stage) return fail(RS_ERR_UNSUPPORTED, "chunk must be >= 4 * q0_stage");
     rs_pipeline *p = new rs_pipeline();
     p->cfg = cfg;
     p->elem = elem;
@@ -511,6 +521,7 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
     K.C = p->cfg.chunk;
     K.qcap = p->cfg.queue_cap;
     K.scap = p->cfg.signal_cap;
+    K.q0_stage = p->cfg.q0_stage;
     K.flags = p->cfg.flags;
     K.tagged = p->cfg.strategy == RS_STRATEGY_TAGGED;
     K.nst = p->nst;
@@ -523,7 +534,7 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
         for (int i = 0; i < 4; ++i) cudaEventCreate(&p->ev[i]);
     p->timed = timing;
     if (timing) cudaEventRecord(p->ev[0], stream);
-    L.pre<<<pre_blocks, 256, 0, stream>>>(K, 4 * (p->nst + 2));
+    L.pre<<<pre_blocks, 256, 0, stream>>>(K, 4 * (MAXK + 2) + 16);
     if (timing) cudaEventRecord(p->ev[1], stream);
     if (seq) L.main<<<p->grid, p->wpb * 32, cta_smem, stream>>>(K);
     else L.ws<<<p->grid, p->wpb * 32, cta_smem, stream>>>(K);
@@ -583,6 +594,16 @@ rs_status rs_pipeline_run_host(rs_pipeline *p, const void *h_elems, int64_t n_el
     if (L.out_bytes1 && cudaMemcpyAsync(h_out.v1, d_o1, (size_t)L.out_bytes1 * (size_t)n_regions, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
         return fail(RS_ERR_CUDA, "D2H aggregates failed");
     if (cudaStreamSynchronize(stream) != cudaSuccess) return fail(RS_ERR_CUDA, "stream synchronize failed");
+    return RS_OK;
+}
+
+rs_status rs_pipeline_profile(rs_pipeline *p, uint64_t *host16, rs_stream stream) {
+    if (!p || !host16) return fail(RS_ERR_INVALID_ARG, "NULL argument");
+    if (!p->last_ws) { std::memset(host16, 0, 16 * sizeof(uint64_t)); return RS_OK; }
+    if (cudaMemcpyAsync(host16, (uint8_t *)p->last_ws + 256 + sizeof(unsigned long long) * 4 * (MAXK + 2),
+                        16 * sizeof(uint64_t), cudaMemcpyDeviceToHost, (cudaStream_t)stream) != cudaSuccess ||
+        cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess)
+        return fail(RS_ERR_CUDA, "profile copy failed");
     return RS_OK;
 }
 

@@ -9,9 +9,12 @@
 // ------------------------------------------------- filter / transform ops
 // isGood() / push() bodies (Fig. 5), specialised per op so the
 // full-ensemble path carries no per-item dispatch (readings A13/A14).
-struct OpHash {
-    uint32_t a, t;
-    __device__ __forceinline__ bool operator()(uint32_t &v) const { return ((v * a) >> 24) < t; }
+struct OpHash {            // keep iff ((v*a) >> 24) < t  <=>  v*a < t << 24   (t <= 255)
+    uint32_t a, tt;
+    __device__ __forceinline__ bool operator()(uint32_t &v) const { return v * a < tt; }
+};
+struct OpAll {             // HASH_LT with t = 256 (or LT_U32 with bound 2^32): keeps every item
+    __device__ __forceinline__ bool operator()(uint32_t &) const { return true; }
 };
 struct OpLt {
     uint32_t b;
@@ -122,8 +125,11 @@ template <int K, int AGG, bool TAG>
 struct Pipe {
     using AT = AggT<AGG>;
     using A = typename AT::A;
-    static constexpr int SBLK = TAG ? 256 : 512;     // elements per TMA stage
-    static constexpr int RING0 = NST * SBLK;         // Q0 ring capacity (items)
+    static constexpr uint32_t default_stage() { return TAG ? 256u : 512u; }
+    // per-instance shared header: [0,32) TMA barriers, [32,128) node counters
+    // (u32 x 24: data firings, full firings, items, signals per node),
+    // [128,256) RS_FLAG_PROFILE cycle counters (u64 x 16)
+    static constexpr uint32_t HDR = 256;
 
     const KParams &P;
     const int lane;
@@ -132,6 +138,7 @@ struct Pipe {
     uint8_t *base;                 // this instance's shared-memory window
     uint64_t *bar;                 // [NST] TMA stage barriers
     uint32_t qmask, smask, qcap, scap;
+    uint32_t sblk, ring0;          // Q0: TMA stage size (elements) and ring capacity (NST stages)
 
     // Edge e (node e -> node e+1).  Kept as named scalars (not arrays) so the
     // whole state lives in registers.
@@ -143,9 +150,6 @@ struct Pipe {
         bool xfer;             // the head signal's credit already moved into cur
     };
     EdgeS E0, E1, E2, E3, E4;
-    // per-node stats: ensembles, full ensembles, items, signals
-    struct NodeS { uint32_t nd, nf, ni, ns; };
-    NodeS N0, N1, N2, N3, N4, N5;
 
     template <int e> __device__ __forceinline__ EdgeS &E() {
         static_assert(e >= 0 && e <= 4, "edge index");
@@ -155,23 +159,25 @@ struct Pipe {
     template <int e> __device__ __forceinline__ const EdgeS &E() const {
         return const_cast<Pipe *>(this)->template E<e>();
     }
-    template <int n> __device__ __forceinline__ NodeS &N() {
-        static_assert(n >= 0 && n <= 5, "node index");
-        if constexpr (n == 0) return N0; else if constexpr (n == 1) return N1; else if constexpr (n == 2) return N2;
-        else if constexpr (n == 3) return N3; else if constexpr (n == 4) return N4; else return N5;
+    // node counters live in the shared header (lane 0 updates them)
+    __device__ __forceinline__ void stat_add(int n, int f, uint32_t v) const {
+        if (lane == 0) reinterpret_cast<uint32_t *>(base + 32)[4 * n + f] += v;
     }
-    // ring addresses: Q0 (RING0 items) then Q_1..Q_K (qcap items), each followed
+    __device__ __forceinline__ void pcnt(int i, unsigned long long v) const {
+        if (lane == 0) reinterpret_cast<unsigned long long *>(base + 128)[i] += v;
+    }
+    // ring addresses: Q0 (ring0 items) then Q_1..Q_K (qcap items), each followed
     // by its tag ring in the tagged strategy, then the signal rings.
     template <int e> __device__ __forceinline__ uint32_t *Q() const {
-        if constexpr (e == 0) return reinterpret_cast<uint32_t *>(base + 128);
-        else return reinterpret_cast<uint32_t *>(base + 128 + RING0 * 4 * (TAG ? 2 : 1) + (e - 1) * qcap * 4 * (TAG ? 2 : 1));
+        if constexpr (e == 0) return reinterpret_cast<uint32_t *>(base + HDR);
+        else return reinterpret_cast<uint32_t *>(base + HDR + ring0 * 4 * (TAG ? 2 : 1) + (e - 1) * qcap * 4 * (TAG ? 2 : 1));
     }
     template <int e> __device__ __forceinline__ uint32_t *T() const {
         if constexpr (!TAG) return nullptr;
-        else return Q<e>() + (e == 0 ? RING0 : qcap);
+        else return Q<e>() + (e == 0 ? ring0 : qcap);
     }
     template <int e> __device__ __forceinline__ uint2 *S() const {
-        return reinterpret_cast<uint2 *>(base + 128 + RING0 * 4 * (TAG ? 2 : 1) + K * qcap * 4 * (TAG ? 2 : 1)) + e * scap;
+        return reinterpret_cast<uint2 *>(base + HDR + ring0 * 4 * (TAG ? 2 : 1) + K * qcap * 4 * (TAG ? 2 : 1)) + e * scap;
     }
 
     Chunk F0, F1;                      // chunk being enumerated, chunk staged next
@@ -190,17 +196,27 @@ struct Pipe {
     A carry;           // tagged: uniform partial of the carry region
     long long base0, offR, off0;
     uint32_t nchunks;
+    uint32_t q_start[K + 1];       // initial queue positions (edge 0 may start at the chunk-0 pad)
+    // RS_FLAG_PROFILE: cycles spent per node (0 = enumerate, 1..K+1, K+2 = TMA wait)
+    const bool prof;
 
     __device__ __forceinline__ Pipe(const KParams &p, uint8_t *smem, int lane_)
-        : P(p), lane(lane_), lt(lanemask_lt()) {
+        : P(p), lane(lane_), lt(lanemask_lt()), prof((p.flags & RS_FLAG_PROFILE) != 0) {
+
         qcap = P.qcap;
         scap = P.scap;
         qmask = qcap - 1;
         smask = scap - 1;
+        sblk = P.q0_stage;
+        ring0 = NST * sblk;
         base = smem;
         bar = reinterpret_cast<uint64_t *>(smem);
         E0 = E1 = E2 = E3 = E4 = EdgeS{0u, 0u, 0u, 0u, 0u, 0u, false};
-        N0 = N1 = N2 = N3 = N4 = N5 = NodeS{0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int e = 0; e <= K; ++e) q_start[e] = 0u;
+        if (lane == 0)
+            for (int i = 8; i < 64; ++i) reinterpret_cast<uint32_t *>(base)[i] = 0u;   // counters + profile
+        __syncwarp();
         F0.k = F1.k = -1;
         claims_done = enum_done = false;
         stg_j = landed_j = 0;
@@ -217,8 +233,8 @@ struct Pipe {
         nchunks = P.hdr->nchunks;
     }
 
-    __host__ __device__ static constexpr uint32_t smem_bytes(uint32_t qcap, uint32_t scap) {
-        return 128 + RING0 * 4 * (TAG ? 2 : 1) + K * qcap * 4 * (TAG ? 2 : 1) + (TAG ? 0 : (K + 1) * scap * 8);
+    __host__ __device__ static constexpr uint32_t smem_bytes(uint32_t qcap, uint32_t scap, uint32_t sblk) {
+        return HDR + NST * sblk * 4 * (TAG ? 2 : 1) + K * qcap * 4 * (TAG ? 2 : 1) + (TAG ? 0 : (K + 1) * scap * 8);
     }
 
     // ---------------------------------------------------------- chunks
@@ -242,13 +258,13 @@ struct Pipe {
         return k < nchunks ? (int32_t)k : -1;
     }
 
-    // Issue TMA stage stg_j (positions [j*SBLK, (j+1)*SBLK)) from chunk c.
+    // Issue TMA stage stg_j (positions [j*sblk, (j+1)*sblk)) from chunk c.
     __device__ __forceinline__ void issue_stage(const Chunk &c) {
         const uint32_t j = stg_j;
-        const uint32_t p0 = j * SBLK;
-        const uint32_t n = min((uint32_t)SBLK, c.pos + flen(c) - p0);
+        const uint32_t p0 = j * sblk;
+        const uint32_t n = min(sblk, c.pos + flen(c) - p0);
         const long long src = c.beg + (long long)p0 - (long long)c.pos;   // 16-byte aligned element index
-        uint32_t *dst = Q<0>() + (p0 & (RING0 - 1));
+        uint32_t *dst = Q<0>() + (p0 & (ring0 - 1));
         uint64_t *b = &bar[j % NST];
         const long long lim = (P.n_elems - src) & ~3ll;     // whole 16-byte blocks inside the array
         const uint32_t ntma = (uint32_t)min((long long)((n + 3u) & ~3u), lim);
@@ -272,8 +288,8 @@ struct Pipe {
     // Keep the Q0 ring full: prefetch element blocks ahead of the enumerate node.
     __device__ __forceinline__ void refill() {
         for (;;) {
-            if ((stg_j + 1) * (uint32_t)SBLK > E<0>().qh + RING0) return;   // ring slots still in use
-            const uint32_t sp = stg_j * SBLK;
+            if ((stg_j + 1) * sblk > E<0>().qh + ring0) return;   // ring slots still in use
+            const uint32_t sp = stg_j * sblk;
             if (F0.k >= 0 && sp < F0.pos + flen(F0)) { issue_stage(F0); continue; }
             if (F1.k >= 0 && sp < F1.pos + flen(F1)) { issue_stage(F1); continue; }
             if (F1.k >= 0 || claims_done) return;
@@ -281,7 +297,7 @@ struct Pipe {
             if (k < 0) { claims_done = true; return; }
             if (F0.k < 0) {
                 const uint32_t pos = (k == 0) ? (uint32_t)(off0 - base0) : sp;
-                if (k == 0 && stg_j == 0) E<0>().qh = E<0>().qt = pos;
+                if (k == 0 && stg_j == 0) { E<0>().qh = E<0>().qt = pos; q_start[0] = pos; }
                 load_chunk(F0, k, pos);
                 pidx = 0;
                 begun = false;
@@ -351,7 +367,7 @@ struct Pipe {
                 prog = true;
                 continue;
             }
-            const uint32_t lim_pos = min(stg_j * (uint32_t)SBLK, F0.pos + flen(F0));
+            const uint32_t lim_pos = min(stg_j * sblk, F0.pos + flen(F0));
             const uint32_t avail = lim_pos - E<0>().qt;
             if (!pc_valid || pidx >= pc_base + 32) {
                 pc_base = pidx;
@@ -360,10 +376,17 @@ struct Pipe {
             }
             const uint32_t d = pidx - pc_base;
             const long long e_next = F0.beg + (long long)(E<0>().qt - F0.pos);
-            if (avail == 0 && (TAG || begun)) {
-                // cheap exit: the current part still has items but nothing is staged
+            if (TAG || begun) {
+                // long part in progress: stream the staged items without the per-part scan
                 const long long pe0 = __shfl_sync(kFull, pc_pe, d);
-                if (pe0 > e_next) return prog;
+                if (pe0 - e_next > (long long)avail) {
+                    if (avail == 0) return prog;
+                    if constexpr (TAG) write_tags_uniform(__shfl_sync(kFull, pc_key, d), avail);
+                    E<0>().qt += avail;
+                    E<0>().sent += avail;
+                    __syncwarp();
+                    return true;
+                }
             }
             long long ps = __shfl_down_sync(kFull, pc_ps, d);
             long long pe = __shfl_down_sync(kFull, pc_pe, d);
@@ -409,13 +432,11 @@ struct Pipe {
                     }
                     const uint32_t nsig = __shfl_sync(kFull, scum, m - 1);
                     E<0>().st += nsig;
-                    N<0>().ns += nsig;
                     E<0>().sent = 0;
                 } else {
                     write_tags(m, cum, cnt, key, tot);
                 }
                 E<0>().qt += tot;
-                N<0>().ni += tot;
                 pidx += m;
                 begun = false;
                 prog = true;
@@ -430,7 +451,6 @@ struct Pipe {
                 if (!begun) {
                     if (scap - (E<0>().st - E<0>().sh) == 0) return prog;
                     push_signal<0>(key0, false, E<0>().sent);
-                    N<0>().ns++;
                     begun = true;
                     did = true;
                 }
@@ -440,13 +460,11 @@ struct Pipe {
                 if constexpr (TAG) write_tags_uniform(key0, k);
                 E<0>().qt += k;
                 E<0>().sent += k;
-                N<0>().ni += k;
                 did = true;
             }
             if constexpr (!TAG) {
                 if (k == cnt0 && scap - (E<0>().st - E<0>().sh) > 0) {
                     push_signal<0>(key0, true, E<0>().sent);
-                    N<0>().ns++;
                     pidx++;
                     begun = false;
                     did = true;
@@ -479,17 +497,17 @@ struct Pipe {
                 if (cand < (int)m && ex <= rel) lo = cand;
             }
             const uint32_t k = __shfl_sync(kFull, key, lo);
-            if (rel < tot) T<0>()[(E<0>().qt + rel) & (RING0 - 1)] = k;
+            if (rel < tot) T<0>()[(E<0>().qt + rel) & (ring0 - 1)] = k;
         }
     }
     __device__ __forceinline__ void write_tags_uniform(uint32_t key, uint32_t k) {
-        for (uint32_t i = lane; i < k; i += 32) T<0>()[(E<0>().qt + i) & (RING0 - 1)] = key;
+        for (uint32_t i = lane; i < k; i += 32) T<0>()[(E<0>().qt + i) & (ring0 - 1)] = key;
     }
 
     // ---------------------------------------------------------- stages
     __device__ __forceinline__ uint32_t landed_pos() {
         while (landed_j < stg_j && mbar_test_uniform(&bar[landed_j % NST], (landed_j / NST) & 1u)) landed_j++;
-        return landed_j * (uint32_t)SBLK;
+        return landed_j * sblk;
     }
 
     // Receiver admissible count on edge e, applying rule (2b).
@@ -547,8 +565,14 @@ struct Pipe {
         } else {
             const StageP &sp = P.st[n - 1];
             switch (sp.op) {
-                case RS_OP_HASH_LT: filter_full<n>(in, tin, imask, h, nens, OpHash{sp.a, sp.b}); break;
-                case RS_OP_LT_U32: filter_full<n>(in, tin, imask, h, nens, OpLt{sp.b, sp.table[0] != 0}); break;
+                case RS_OP_HASH_LT:
+                    if (sp.b >= 256) filter_full<n>(in, tin, imask, h, nens, OpAll{});
+                    else filter_full<n>(in, tin, imask, h, nens, OpHash{sp.a, sp.b << 24});
+                    break;
+                case RS_OP_LT_U32:
+                    if (sp.table[0]) filter_full<n>(in, tin, imask, h, nens, OpAll{});
+                    else filter_full<n>(in, tin, imask, h, nens, OpLt{sp.b, false});
+                    break;
                 case RS_OP_CLASS: filter_full<n>(in, tin, imask, h, nens, OpClass{sp.table}); break;
                 case RS_OP_SCALE_F32: filter_full<n>(in, tin, imask, h, nens, OpScale{__uint_as_float(sp.a)}); break;
                 default: filter_full<n>(in, tin, imask, h, nens, OpAffine{sp.a, sp.b}); break;
@@ -563,7 +587,7 @@ struct Pipe {
     __device__ __forceinline__ bool fire(bool drained) {
         constexpr int ei = n - 1;          // input edge
         constexpr bool AGGN = (n == K + 1);
-        const uint32_t imask = (ei == 0) ? (RING0 - 1) : qmask;
+        const uint32_t imask = (ei == 0) ? (ring0 - 1) : qmask;
         const uint32_t *in = Q<ei>();
         const uint32_t *tin = T<ei>();
         bool prog = false;
@@ -588,9 +612,7 @@ struct Pipe {
                 run_full<n>(in, tin, imask, E<ei>().qh, nens);
                 E<ei>().qh += nens * W;
                 if (spend) E<ei>().cur -= nens * W;
-                N<n>().nd += nens;
-                N<n>().nf += nens;
-                N<n>().ni += nens * W;
+                stat_add(n, 1, nens);          // full ensembles (items/ensembles derived at exit)
                 prog = true;
                 continue;
             }
@@ -605,8 +627,7 @@ struct Pipe {
                 run_partial<n>(in, tin, imask, E<ei>().qh, e);
                 E<ei>().qh += e;
                 if (spend) E<ei>().cur -= e;
-                N<n>().nd++;
-                N<n>().ni += e;
+                stat_add(n, 0, 1u);            // partial ensembles
                 prog = true;
                 continue;
             }
@@ -624,7 +645,6 @@ struct Pipe {
             }
             E<ei>().sh++;
             E<ei>().xfer = false;
-            N<n>().ns++;
             prog = true;
             const bool is_end = (hs.y & END_BIT) != 0;
             if constexpr (AGGN) {
@@ -753,23 +773,41 @@ struct Pipe {
         if constexpr (n > K + 1) {
             return false;
         } else {
+            const long long t0 = prof ? clock64() : 0;
             const bool p = fire<n>(drained);
+            if (prof) pcnt(n, clock64() - t0);
             const bool dn = drained && (E<n - 1>().qh == E<n - 1>().qt) && (E<n - 1>().sh == E<n - 1>().st);
             return fire_chain<n + 1>(dn) | p;
         }
     }
 
-    template <int n>
-    __device__ __forceinline__ void flush_stats() {
-        if constexpr (n < K + 2) {
-            if (lane == n) {
-                unsigned long long *S = P.stats + 4 * n;
-                if (N<n>().nd) atomicAdd(S + 0, (unsigned long long)N<n>().nd);
-                if (N<n>().nf) atomicAdd(S + 1, (unsigned long long)N<n>().nf);
-                if (N<n>().ni) atomicAdd(S + 2, (unsigned long long)N<n>().ni);
-                if (N<n>().ns) atomicAdd(S + 3, (unsigned long long)N<n>().ns);
+    // Node n's items = positions it consumed on edge n-1; its data firings =
+    // full ensembles + partial ensembles (counted separately in the header).
+    template <int n = 1>
+    __device__ __forceinline__ void finish_counters() {
+        if constexpr (n <= K + 1) {
+            if (lane == 0) {
+                uint32_t *c = reinterpret_cast<uint32_t *>(base + 32) + 4 * n;
+                c[0] += c[1];
+                c[2] = E<n - 1>().qh - q_start[n - 1];
+                c[3] = E<n - 1>().sh;                      // signals consumed
+                if constexpr (n == 1) {                     // enumerate: items / signals emitted
+                    c[-4 + 2] = E<0>().qt - q_start[0];
+                    c[-4 + 3] = E<0>().st;
+                }
             }
-            flush_stats<n + 1>();
+            finish_counters<n + 1>();
+        }
+    }
+    __device__ __forceinline__ void flush_stats() {
+        finish_counters<1>();
+        __syncwarp();
+        if (lane < K + 2) {
+            const uint32_t *c = reinterpret_cast<const uint32_t *>(base + 32) + 4 * lane;
+            unsigned long long *S = P.stats + 4 * lane;
+#pragma unroll
+            for (int f = 0; f < 4; ++f)
+                if (c[f]) atomicAdd(S + f, (unsigned long long)c[f]);
         }
     }
 
@@ -780,12 +818,15 @@ struct Pipe {
         __syncwarp();
         uint32_t idle = 0;
         for (;;) {
+            const long long t0 = prof ? clock64() : 0;
             bool prog = enumerate();
+            if (prof) { pcnt(0, clock64() - t0); pcnt(8, 1); }
             prog |= fire_chain<1>(enum_done);
             if (enum_done && all_empty()) break;
             if (prog) { idle = 0; continue; }
             // nothing fireable: wait for the oldest in-flight TMA stage
             if (landed_j < stg_j) {
+                const long long tw = prof ? clock64() : 0;
                 uint32_t spins = 0;
                 while (!mbar_try_wait_uniform(&bar[landed_j % NST], (landed_j / NST) & 1u)) {
                     if (++spins > (1u << 24)) break;
@@ -794,6 +835,7 @@ struct Pipe {
                     if (lane == 0) atomicCAS((int *)&P.hdr->err, 0, ERR_WATCHDOG);
                     break;
                 }
+                if (prof) { pcnt(K + 2, clock64() - tw); pcnt(9, 1); }
                 continue;
             }
             if (++idle > 64) {
@@ -806,7 +848,15 @@ struct Pipe {
         for (uint32_t spins = 0; landed_j < stg_j && spins < (1u << 26); ++spins) {
             if (mbar_try_wait_uniform(&bar[landed_j % NST], (landed_j / NST) & 1u)) landed_j++;
         }
-        if (P.flags & RS_FLAG_STATS) flush_stats<0>();
+        __syncwarp();
+        if (P.flags & RS_FLAG_STATS) flush_stats();
+        if (prof && lane == 0) {
+            // per-node cycles (enumerate, nodes 1..K+1, TMA wait), sweeps, waits
+            unsigned long long *Pr = P.stats + 4 * (MAXK + 2);
+            const unsigned long long *c = reinterpret_cast<const unsigned long long *>(base + 128);
+            for (int i = 0; i < 10; ++i) atomicAdd(Pr + i, c[i]);
+            atomicAdd(Pr + 10, 1ull);
+        }
     }
 };
 
@@ -816,7 +866,7 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_pipeline(const __grid_constant_
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     using PP = Pipe<K, AGG, TAG>;
-    uint8_t *mine = smem + (size_t)warp * PP::smem_bytes(P.qcap, P.scap);
+    uint8_t *mine = smem + (size_t)warp * PP::smem_bytes(P.qcap, P.scap, P.q0_stage);
     if (P.hdr->err) return;
     PP pipe(P, mine, lane);
     pipe.run();

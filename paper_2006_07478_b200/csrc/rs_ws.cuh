@@ -612,8 +612,14 @@ struct WS {
     __device__ void run_stage(int n) const {
         const StageP &sp = P.st[n - 1];
         switch (sp.op) {
-            case RS_OP_HASH_LT: run_stage_op(n, OpHash{sp.a, sp.b}); break;
-            case RS_OP_LT_U32: run_stage_op(n, OpLt{sp.b, sp.table[0] != 0}); break;
+            case RS_OP_HASH_LT:
+                if (sp.b >= 256) run_stage_op(n, OpAll{});
+                else run_stage_op(n, OpHash{sp.a, sp.b << 24});
+                break;
+            case RS_OP_LT_U32:
+                if (sp.table[0]) run_stage_op(n, OpAll{});
+                else run_stage_op(n, OpLt{sp.b, false});
+                break;
             case RS_OP_CLASS: run_stage_op(n, OpClass{sp.table}); break;
             case RS_OP_SCALE_F32: run_stage_op(n, OpScale{__uint_as_float(sp.a)}); break;
             default: run_stage_op(n, OpAffine{sp.a, sp.b}); break;

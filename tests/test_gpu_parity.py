@@ -30,7 +30,7 @@ def rs():
     return rs
 
 
-def run_gpu(rs, vals, off, stages, agg, strategy="signal", mode="ws", **cfg):
+def run_gpu(rs, vals, off, stages, agg, strategy="signal", mode="seq", **cfg):
     flags = rs.RS_FLAG_STATS | (rs.RS_FLAG_WARP_SPECIALIZED if mode == "ws" else 0)
     p = rs.Pipeline(stages, agg, strategy=strategy, flags=flags, **cfg)
     dev = torch.device("cuda:0")
