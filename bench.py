@@ -285,17 +285,17 @@ def run_ours(args):
         gather_buf = [torch.empty_like(out[0]) for _ in range(world)]
 
     # ---- device-timed region: W warm-ups, then K steps, barrier + sync both sides
-    for _ in range(args.warmup):
-        p.run(vals, off, out, ws)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     stream = torch.cuda.current_stream()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     main_ms = []
     with Clocks(local) as clk:
-        clk.wait_ready()
+        clk.wait_ready()                 # sampler running before the warm-up
+        for _ in range(args.warmup):
+            p.run(vals, off, out, ws)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         w0 = time.time()
         t0.record(stream)

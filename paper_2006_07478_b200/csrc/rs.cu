@@ -77,6 +77,7 @@ struct KParams {
     uint32_t C;                     // chunk length (children)
     uint32_t qcap, scap;            // queue / signal capacities (powers of 2)
     uint32_t q0_stage;              // Q0 TMA stage size in elements (sequential kernel)
+    uint32_t esize;                 // element size in bytes (1 = u8 text, else 4)
     uint32_t flags;
     int32_t tagged;
     int32_t nst;
@@ -108,8 +109,8 @@ __global__ void k_prepass(KParams P, int n_stats) {
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nth = (long long)gridDim.x * blockDim.x;
     const long long off0 = P.off[0], offR = P.off[P.R];
-    const long long align = 16;  // bytes; element size 4 -> 4 elements
-    const long long esz = 4;
+    const long long align = 16;  // bytes: TMA copies whole 16-byte blocks
+    const long long esz = P.esize;
     const long long base0 = (off0 * esz / align) * align / esz;
     long long span = offR - base0;
     long long nch = span <= 0 ? 1 : (span + P.C - 1) / P.C;
@@ -289,6 +290,7 @@ bool get_launch(const rs_pipeline *p, Launch *L) {
         case RS_OP_SUM_I64: *L = launch_for<20>(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
         case RS_OP_SUM_F32: *L = launch_for<21>(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
         case RS_OP_COUNT_MIN_U32: *L = launch_for<22>(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
+        case RS_OP_COUNT_XOR64: *L = launch_for<23>(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
     }
     return false;
 }
@@ -369,7 +371,11 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
         case RS_OP_SUM_I64: if (elem != RS_I32) return fail(RS_ERR_UNSUPPORTED, "SUM_I64 needs i32 elements"); break;
         case RS_OP_SUM_F32: if (elem != RS_F32) return fail(RS_ERR_UNSUPPORTED, "SUM_F32 needs f32 elements"); break;
         case RS_OP_COUNT_MIN_U32: if (elem != RS_U32) return fail(RS_ERR_UNSUPPORTED, "COUNT_MIN_U32 needs u32 elements"); break;
-        case RS_OP_COUNT_XOR64: return fail(RS_ERR_UNSUPPORTED, "COUNT_XOR64 (u8 text) is not built yet");
+        case RS_OP_COUNT_XOR64:
+            if (elem != RS_U8) return fail(RS_ERR_UNSUPPORTED, "COUNT_XOR64 needs u8 elements");
+            if (cfg_in && (cfg_in->flags & RS_FLAG_WARP_SPECIALIZED))
+                return fail(RS_ERR_UNSUPPORTED, "COUNT_XOR64 is built for the sequential scheduler only");
+            break;
         default: return fail(RS_ERR_UNSUPPORTED, "unknown aggregate op");
     }
     if (cfg.strategy != RS_STRATEGY_SIGNAL && cfg.strategy != RS_STRATEGY_TAGGED)
@@ -522,6 +528,7 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
     K.qcap = p->cfg.queue_cap;
     K.scap = p->cfg.signal_cap;
     K.q0_stage = p->cfg.q0_stage;
+    K.esize = p->elem == RS_U8 ? 1u : 4u;
     K.flags = p->cfg.flags;
     K.tagged = p->cfg.strategy == RS_STRATEGY_TAGGED;
     K.nst = p->nst;

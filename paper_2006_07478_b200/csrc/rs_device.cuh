@@ -110,6 +110,7 @@ struct AggT<20> {  // RS_OP_SUM_I64 over int32 elements
     using A = unsigned long long;  // two's-complement wraparound sum
     __device__ static A id() { return 0ull; }
     __device__ static A lift(uint32_t v) { return (A)(long long)(int)v; }
+    __device__ static A lift_i(uint32_t v, long long) { return lift(v); }
     __device__ static A comb(A a, A b) { return a + b; }
     __device__ static A shfl(A a, int src) { return __shfl_sync(kFull, a, src); }
     __device__ static A shfl_up(A a, int d) { return __shfl_up_sync(kFull, a, d); }
@@ -124,6 +125,7 @@ struct AggT<21> {  // RS_OP_SUM_F32 over fp32 elements
     using A = float;
     __device__ static A id() { return 0.0f; }
     __device__ static A lift(uint32_t v) { return __uint_as_float(v); }
+    __device__ static A lift_i(uint32_t v, long long) { return lift(v); }
     __device__ static A comb(A a, A b) { return __fadd_rn(a, b); }
     __device__ static A shfl(A a, int src) { return __shfl_sync(kFull, a, src); }
     __device__ static A shfl_up(A a, int d) { return __shfl_up_sync(kFull, a, d); }
@@ -138,6 +140,7 @@ struct AggT<22> {  // RS_OP_COUNT_MIN_U32 over uint32 elements: (count, min)
     using A = uint2;
     __device__ static A id() { return make_uint2(0u, 0xffffffffu); }
     __device__ static A lift(uint32_t v) { return make_uint2(1u, v); }
+    __device__ static A lift_i(uint32_t v, long long) { return lift(v); }
     __device__ static A comb(A a, A b) { return make_uint2(a.x + b.x, min(a.y, b.y)); }
     __device__ static A shfl(A a, int src) {
         return make_uint2(__shfl_sync(kFull, a.x, src), __shfl_sync(kFull, a.y, src));
@@ -156,6 +159,44 @@ struct AggT<22> {  // RS_OP_COUNT_MIN_U32 over uint32 elements: (count, min)
         return make_uint2(((const uint32_t *)o0)[i], ((const uint32_t *)o1)[i]);
     }
     static constexpr int bytes0 = 4, bytes1 = 4;
+};
+
+// splitmix64 finalizer (reading A19: the text aggregate hashes (i << 8 | byte)).
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+template <>
+struct AggT<23> {  // RS_OP_COUNT_XOR64 over u8 elements: (count, xor of mix64(i << 8 | byte))
+    using A = ulonglong2;
+    __device__ static A id() { return make_ulonglong2(0ull, 0ull); }
+    // item = byte | (position mod C) << 8; delta = chunk base - region start, so the
+    // byte's index within its region is i = delta + (item >> 8)
+    __device__ static A lift_i(uint32_t v, long long delta) {
+        const unsigned long long i = (unsigned long long)(delta + (long long)(v >> 8));
+        return make_ulonglong2(1ull, mix64((i << 8) | (v & 0xffu)));
+    }
+    __device__ static A lift(uint32_t v) { return lift_i(v, 0); }   // (index-free form; unused)
+    __device__ static A comb(A a, A b) { return make_ulonglong2(a.x + b.x, a.y ^ b.y); }
+    __device__ static A shfl(A a, int src) {
+        return make_ulonglong2(__shfl_sync(kFull, a.x, src), __shfl_sync(kFull, a.y, src));
+    }
+    __device__ static A shfl_up(A a, int d) {
+        return make_ulonglong2(__shfl_up_sync(kFull, a.x, d), __shfl_up_sync(kFull, a.y, d));
+    }
+    __device__ static A shfl_xor(A a, int m) {
+        return make_ulonglong2(__shfl_xor_sync(kFull, a.x, m), __shfl_xor_sync(kFull, a.y, m));
+    }
+    __device__ static void store(void *o0, void *o1, uint64_t i, A a) {
+        ((unsigned long long *)o0)[i] = a.x;
+        ((unsigned long long *)o1)[i] = a.y;
+    }
+    __device__ static A load(const void *o0, const void *o1, uint64_t i) {
+        return make_ulonglong2(((const unsigned long long *)o0)[i], ((const unsigned long long *)o1)[i]);
+    }
+    static constexpr int bytes0 = 8, bytes1 = 8;
 };
 
 template <class AT>

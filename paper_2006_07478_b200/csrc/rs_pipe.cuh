@@ -46,17 +46,32 @@ struct OpAffine {
 // NS slices (NS*32 items, one or two ensembles) are processed together: all
 // loads first, then the predicates, then the stable ballot/popc compaction
 // into the output queue (push) -- NS-way instruction-level parallelism.
-template <bool TAG, int NS, class Op>
+// Items are 32-bit.  A byte element ring (U8IN, the text stream) is read as
+// item = byte | (position mod C) << 8: the position within the chunk lets the
+// aggregate recover each byte's index within its line (reading A19).
+template <bool U8IN>
+__device__ __forceinline__ uint32_t load_item(const uint32_t *in, uint32_t pos, uint32_t imask, uint32_t cmask) {
+    if constexpr (U8IN) return (uint32_t)reinterpret_cast<const uint8_t *>(in)[pos & imask] | ((pos & cmask) << 8);
+    else return in[pos & imask];
+}
+
+template <bool TAG, int NS, class Op, bool U8IN>
 __device__ __forceinline__ void filter_slices(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                               uint32_t *out, uint32_t *tout, uint32_t qmask, uint32_t &tl,
-                                              const Op &op, uint32_t lt) {
+                                              const Op &op, uint32_t lt, uint32_t cmask) {
     const uint32_t lane = threadIdx.x & 31u;
     uint32_t v[NS], tg[NS];
     bool keep[NS];
     if (((h & imask) + NS * 32) <= imask + 1) {        // input range does not wrap the ring
-        const uint32_t *src = in + (h & imask) + lane;
+        if constexpr (U8IN) {
+            const uint8_t *src8 = reinterpret_cast<const uint8_t *>(in) + (h & imask) + lane;
 #pragma unroll
-        for (int j = 0; j < NS; ++j) v[j] = src[32 * j];
+            for (int j = 0; j < NS; ++j) v[j] = (uint32_t)src8[32 * j] | (((h + 32 * j + lane) & cmask) << 8);
+        } else {
+            const uint32_t *src = in + (h & imask) + lane;
+#pragma unroll
+            for (int j = 0; j < NS; ++j) v[j] = src[32 * j];
+        }
         if constexpr (TAG) {
             const uint32_t *ts = tin + (h & imask) + lane;
 #pragma unroll
@@ -64,7 +79,7 @@ __device__ __forceinline__ void filter_slices(const uint32_t *in, const uint32_t
         }
     } else {
 #pragma unroll
-        for (int j = 0; j < NS; ++j) v[j] = in[(h + 32 * j + lane) & imask];
+        for (int j = 0; j < NS; ++j) v[j] = load_item<U8IN>(in, h + 32 * j + lane, imask, cmask);
         if constexpr (TAG) {
 #pragma unroll
             for (int j = 0; j < NS; ++j) tg[j] = tin[(h + 32 * j + lane) & imask];
@@ -102,13 +117,14 @@ __device__ __forceinline__ void filter_slices(const uint32_t *in, const uint32_t
     }
 }
 
-template <bool TAG, class Op>
+template <bool TAG, class Op, bool U8IN = false>
 __device__ __noinline__ uint32_t filter_batch(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                               uint32_t nens, uint32_t *out, uint32_t *tout, uint32_t qmask,
-                                              uint32_t tl, const Op op, uint32_t lt) {
+                                              uint32_t tl, const Op op, uint32_t lt, uint32_t cmask = 0) {
     uint32_t k = 0;
-    for (; k + 2 <= nens; k += 2, h += 2 * W) filter_slices<TAG, 2 * IPL>(in, tin, imask, h, out, tout, qmask, tl, op, lt);
-    if (k < nens) filter_slices<TAG, IPL>(in, tin, imask, h, out, tout, qmask, tl, op, lt);
+    for (; k + 2 <= nens; k += 2, h += 2 * W)
+        filter_slices<TAG, 2 * IPL, Op, U8IN>(in, tin, imask, h, out, tout, qmask, tl, op, lt, cmask);
+    if (k < nens) filter_slices<TAG, IPL, Op, U8IN>(in, tin, imask, h, out, tout, qmask, tl, op, lt, cmask);
     __syncwarp();
     return tl;
 }
@@ -126,6 +142,9 @@ struct Pipe {
     using AT = AggT<AGG>;
     using A = typename AT::A;
     static constexpr uint32_t default_stage() { return TAG ? 256u : 512u; }
+    static constexpr bool U8 = (AGG == 23);          // text stream: byte elements
+    static constexpr uint32_t ESZ = U8 ? 1u : 4u;    // element size in the Q0 ring (bytes)
+    __host__ __device__ static constexpr uint32_t q0_bytes(uint32_t sblk) { return (NST * sblk * ESZ + 15u) & ~15u; }
     // per-instance shared header: [0,32) TMA barriers, [32,128) node counters
     // (u32 x 24: data firings, full firings, items, signals per node),
     // [128,256) RS_FLAG_PROFILE cycle counters (u64 x 16)
@@ -170,14 +189,17 @@ struct Pipe {
     // by its tag ring in the tagged strategy, then the signal rings.
     template <int e> __device__ __forceinline__ uint32_t *Q() const {
         if constexpr (e == 0) return reinterpret_cast<uint32_t *>(base + HDR);
-        else return reinterpret_cast<uint32_t *>(base + HDR + ring0 * 4 * (TAG ? 2 : 1) + (e - 1) * qcap * 4 * (TAG ? 2 : 1));
+        else return reinterpret_cast<uint32_t *>(base + HDR + q0_bytes(sblk) + (TAG ? ring0 * 4 : 0) +
+                                                 (e - 1) * qcap * 4 * (TAG ? 2 : 1));
     }
     template <int e> __device__ __forceinline__ uint32_t *T() const {
         if constexpr (!TAG) return nullptr;
-        else return Q<e>() + (e == 0 ? ring0 : qcap);
+        else if constexpr (e == 0) return reinterpret_cast<uint32_t *>(base + HDR + q0_bytes(sblk));
+        else return Q<e>() + qcap;
     }
     template <int e> __device__ __forceinline__ uint2 *S() const {
-        return reinterpret_cast<uint2 *>(base + HDR + ring0 * 4 * (TAG ? 2 : 1) + K * qcap * 4 * (TAG ? 2 : 1)) + e * scap;
+        return reinterpret_cast<uint2 *>(base + HDR + q0_bytes(sblk) + (TAG ? ring0 * 4 : 0) + K * qcap * 4 * (TAG ? 2 : 1)) +
+               e * scap;
     }
 
     Chunk F0, F1;                      // chunk being enumerated, chunk staged next
@@ -194,6 +216,8 @@ struct Pipe {
     A acc;             // per-lane partial accumulator
     uint32_t akey;     // tagged: key of the running (carry) region; 0xffffffff = none
     A carry;           // tagged: uniform partial of the carry region
+    long long adelta;  // text aggregate: index offset of the current part (see part_delta)
+    uint32_t dkey;     // tagged text aggregate: key whose delta is cached in adelta (per lane)
     long long base0, offR, off0;
     uint32_t nchunks;
     uint32_t q_start[K + 1];       // initial queue positions (edge 0 may start at the chunk-0 pad)
@@ -227,6 +251,8 @@ struct Pipe {
         acc = AT::id();
         carry = AT::id();
         akey = 0xffffffffu;
+        adelta = 0;
+        dkey = 0xffffffffu;
         base0 = P.hdr->base0;
         offR = P.hdr->offR;
         off0 = P.hdr->off0;
@@ -234,7 +260,8 @@ struct Pipe {
     }
 
     __host__ __device__ static constexpr uint32_t smem_bytes(uint32_t qcap, uint32_t scap, uint32_t sblk) {
-        return HDR + NST * sblk * 4 * (TAG ? 2 : 1) + K * qcap * 4 * (TAG ? 2 : 1) + (TAG ? 0 : (K + 1) * scap * 8);
+        return HDR + q0_bytes(sblk) + (TAG ? NST * sblk * 4 : 0) + K * qcap * 4 * (TAG ? 2 : 1) +
+               (TAG ? 0 : (K + 1) * scap * 8);
     }
 
     // ---------------------------------------------------------- chunks
@@ -260,24 +287,28 @@ struct Pipe {
 
     // Issue TMA stage stg_j (positions [j*sblk, (j+1)*sblk)) from chunk c.
     __device__ __forceinline__ void issue_stage(const Chunk &c) {
+        constexpr uint32_t AL = 16u / ESZ;                     // elements per 16-byte block
         const uint32_t j = stg_j;
         const uint32_t p0 = j * sblk;
         const uint32_t n = min(sblk, c.pos + flen(c) - p0);
         const long long src = c.beg + (long long)p0 - (long long)c.pos;   // 16-byte aligned element index
-        uint32_t *dst = Q<0>() + (p0 & (ring0 - 1));
+        uint8_t *dst = reinterpret_cast<uint8_t *>(Q<0>()) + (size_t)(p0 & (ring0 - 1)) * ESZ;
         uint64_t *b = &bar[j % NST];
-        const long long lim = (P.n_elems - src) & ~3ll;     // whole 16-byte blocks inside the array
-        const uint32_t ntma = (uint32_t)min((long long)((n + 3u) & ~3u), lim);
+        const long long lim = (P.n_elems - src) & ~(long long)(AL - 1);   // whole 16-byte blocks in the array
+        const uint32_t ntma = (uint32_t)min((long long)((n + AL - 1) & ~(AL - 1)), lim);
         // tail elements that a 16-byte copy cannot reach without overrunning n_elems
         const int tail = (int)n - (int)ntma;
-        if (tail > 0 && lane < tail)
-            dst[ntma + lane] = __ldg(reinterpret_cast<const uint32_t *>(P.elems) + src + ntma + lane);
+        if (tail > 0 && lane < tail) {
+            if constexpr (U8) dst[ntma + lane] = P.elems[src + ntma + lane];
+            else reinterpret_cast<uint32_t *>(dst)[ntma + lane] =
+                __ldg(reinterpret_cast<const uint32_t *>(P.elems) + src + ntma + lane);
+        }
         __syncwarp();
         if (lane == 0) {
             fence_proxy_async();
             if (ntma) {
-                mbar_arrive_expect_tx(b, ntma * 4u);
-                tma_load_1d(dst, P.elems + src * 4, ntma * 4u, b);
+                mbar_arrive_expect_tx(b, ntma * ESZ);
+                tma_load_1d(dst, P.elems + src * ESZ, ntma * ESZ, b);
             } else {
                 mbar_arrive(b);
             }
@@ -526,25 +557,48 @@ struct Pipe {
     template <int n, class Op>
     __device__ __forceinline__ void filter_full(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                                 uint32_t nens, const Op op) {
-        const uint32_t tl = filter_batch<TAG, Op>(in, tin, imask, h, nens, Q<n>(), T<n>(), qmask, E<n>().qt, op, lt);
+        const uint32_t tl = filter_batch<TAG, Op, U8 && n == 1>(in, tin, imask, h, nens, Q<n>(), T<n>(), qmask,
+                                                               E<n>().qt, op, lt, P.C - 1);
         E<n>().sent += tl - E<n>().qt;
         E<n>().qt = tl;
+    }
+
+    static constexpr bool AGG_U8IN = U8 && K == 0;     // aggregate reads the byte ring directly
+    __device__ __forceinline__ uint32_t agg_load(const uint32_t *in, uint32_t pos, uint32_t imask) const {
+        return load_item<AGG_U8IN>(in, pos, imask, P.C - 1);
+    }
+
+    // Index-within-region offset of a part (text aggregate): delta = chunk base
+    // - region start, so i = delta + (item >> 8).
+    __device__ __forceinline__ long long part_delta(uint32_t key) const {
+        uint32_t r;
+        long long cb;
+        if (key & SLOT) {
+            const uint32_t slot = key & ~SLOT, k = slot >> 1;
+            r = ((slot & 1u) ? P.chunk_fr[k + 1] : P.chunk_fr[k]) - 1u;
+            cb = base0 + (long long)k * P.C;
+        } else {
+            r = key;
+            const long long k = (P.off[r] - base0) / P.C;
+            cb = base0 + k * P.C;
+        }
+        return cb - P.off[r];
     }
 
     template <int NS>
     __device__ __forceinline__ void agg_slices(const uint32_t *in, uint32_t imask, uint32_t h) {
         uint32_t v[NS];
-        if (((h & imask) + NS * 32) <= imask + 1) {
+        if (!AGG_U8IN && ((h & imask) + NS * 32) <= imask + 1) {
             const uint32_t *src = in + (h & imask) + lane;
 #pragma unroll
             for (int j = 0; j < NS; ++j) v[j] = src[32 * j];
         } else {
 #pragma unroll
-            for (int j = 0; j < NS; ++j) v[j] = in[(h + 32 * j + lane) & imask];
+            for (int j = 0; j < NS; ++j) v[j] = agg_load(in, h + 32 * j + lane, imask);
         }
-        A part = AT::lift(v[0]);
+        A part = AT::lift_i(v[0], adelta);
 #pragma unroll
-        for (int j = 1; j < NS; ++j) part = AT::comb(part, AT::lift(v[j]));
+        for (int j = 1; j < NS; ++j) part = AT::comb(part, AT::lift_i(v[j], adelta));
         acc = AT::comb(acc, part);
     }
     __device__ __forceinline__ void agg_full(const uint32_t *in, uint32_t imask, uint32_t h, uint32_t nens) {
@@ -650,6 +704,7 @@ struct Pipe {
             if constexpr (AGGN) {
                 if (!is_end) {               // a::begin: acc = identity
                     acc = AT::id();
+                    if constexpr (U8) adelta = part_delta(hs.x);
                 } else {                     // a::end: push(acc)
                     const A v = warp_reduce<AT>(acc);
                     if (lane == 0) store_key(hs.x, v);
@@ -677,7 +732,7 @@ struct Pipe {
 #pragma unroll
                 for (int j = 0; j < IPL; ++j) {
                     const uint32_t idx = j * 32 + lane;
-                    if (idx < e) acc = AT::comb(acc, AT::lift(in[(h + idx) & imask]));
+                    if (idx < e) acc = AT::comb(acc, AT::lift_i(agg_load(in, h + idx, imask), adelta));
                 }
             } else {
                 agg_tagged(in, tin, imask, h, e);
@@ -691,7 +746,7 @@ struct Pipe {
             for (int j = 0; j < IPL; ++j) {
                 const uint32_t idx = j * 32 + lane;
                 const bool act = idx < e;
-                uint32_t v = act ? in[(h + idx) & imask] : 0u;
+                uint32_t v = act ? load_item<U8 && n == 1>(in, h + idx, imask, P.C - 1) : 0u;
                 uint32_t tg = 0;
                 if constexpr (TAG) tg = act ? tin[(h + idx) & imask] : 0u;
                 const bool keep = act && stage_apply(sp, v);
@@ -720,7 +775,10 @@ struct Pipe {
             const bool act = lane < cntj;
             const uint32_t idx = j * 32 + lane;
             const uint32_t key = act ? tin[(h + idx) & imask] : 0xffffffffu;
-            const A val = act ? AT::lift(in[(h + idx) & imask]) : AT::id();
+            if constexpr (U8) {
+                if (act && key != dkey) { dkey = key; adelta = part_delta(key); }
+            }
+            const A val = act ? AT::lift_i(agg_load(in, h + idx, imask), adelta) : AT::id();
             if (__all_sync(kFull, !act || key == akey)) {
                 acc = AT::comb(acc, val);      // fast path: the whole slice continues the carry region
                 continue;

@@ -11,6 +11,11 @@ Workload recipes:
               int32 full range, 3 x HASH_LT(T=192), SUM_I64; fp32 variant
               U[0,1) with SUM_F32.  Fixed-children reading N = 2^29 (the
               paper's 512M integers).
+  D4 text   : i.i.d. bytes: '\n' with p = 1/1397 (geometric lines of mean
+              1397 chars), '{' with p = 45/1397 (~45 per line,
+              P:681-682), digits with p = 1/2, other printable bytes
+              otherwise; lines are CSR regions ending with their '\n'
+              (reading A20); CLASS('{') filter, COUNT_XOR64.
   D5 zipf   : lengths Zipf(s=1.2) on [1, 4096], int32, sweep filters, SUM_I64.
 """
 from __future__ import annotations
@@ -28,6 +33,22 @@ def sweep_stages(n: int = 3, T: int = HASH_T):
 
 def tiny_stages():
     return sweep_stages(2)
+
+
+def class_table(chars: bytes) -> bytes:
+    """32-byte bitmap of a byte class (CLASS filter)."""
+    t = bytearray(32)
+    for c in chars:
+        t[c >> 3] |= 1 << (c & 7)
+    return bytes(t)
+
+
+TEXT_CLASS = class_table(b"{")
+_OTHER = np.frombuffer(b"abcdefghijklmnopqrstuvwxyzABCDEFGHIJKLMNOPQRSTUVWXYZ,.:;-_ }[]\"/=+", np.uint8)
+
+
+def text_stages():
+    return [("class", TEXT_CLASS)]
 
 
 # ----------------------------------------------------------------- numpy side
@@ -78,6 +99,25 @@ def values(N: int, dtype: str, seed: int = 0) -> np.ndarray:
     if dtype == "u8":
         return g.integers(0, 256, size=N, dtype=np.uint8)
     raise ValueError(dtype)
+
+
+def text(N: int, seed: int = 0, line_mean: float = 1397.0, brace_per_line: float = 45.0, base: int = 0):
+    """D4 byte stream (numpy).  Returns (bytes u8[N], offsets int64[R+1]) with
+    every line ending at its newline; a final unterminated line is a region."""
+    g = _rng(seed)
+    u = g.random(N)
+    p_nl = 1.0 / line_mean
+    p_br = brace_per_line / line_mean
+    b = np.empty(N, np.uint8)
+    other = _OTHER[g.integers(0, _OTHER.size, size=N)]
+    digits = (ord("0") + g.integers(0, 10, size=N)).astype(np.uint8)
+    b[:] = np.where(u < 0.5, digits, other)
+    b[u < p_br + p_nl] = ord("{")
+    b[u < p_nl] = ord("\n")
+    nl = np.nonzero(b == ord("\n"))[0] + 1
+    ends = nl if (nl.size and nl[-1] == N) else np.concatenate([nl, [N]])
+    off = np.concatenate([[0], ends]).astype(np.int64) + base
+    return b, off
 
 
 def tiny(seed: int = 0x5EED + 1):
@@ -132,6 +172,27 @@ def torch_values(N: int, dtype: str, seed: int = 0, device="cuda"):
     if dtype == "u8":
         return torch.randint(0, 256, (N,), generator=g, device=device, dtype=torch.uint8)
     raise ValueError(dtype)
+
+
+def torch_text(N: int, seed: int = 0, device="cuda", line_mean: float = 1397.0, brace_per_line: float = 45.0):
+    """D4 byte stream generated on the device (same recipe as text())."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    u = torch.rand(N, generator=g, device=device, dtype=torch.float32)
+    other = torch.from_numpy(_OTHER.copy()).to(device)
+    pick = torch.randint(0, other.numel(), (N,), generator=g, device=device, dtype=torch.int32)
+    digit = torch.randint(ord("0"), ord("9") + 1, (N,), generator=g, device=device, dtype=torch.int32).to(torch.uint8)
+    b = torch.where(u < 0.5, digit, other[pick])
+    p_nl = 1.0 / line_mean
+    b[u < p_nl + brace_per_line / line_mean] = ord("{")
+    b[u < p_nl] = ord("\n")
+    del u, pick, digit
+    nl = torch.nonzero(b == ord("\n")).flatten().to(torch.int64) + 1
+    if nl.numel() == 0 or int(nl[-1].item()) != N:
+        nl = torch.cat([nl, torch.tensor([N], dtype=torch.int64, device=device)])
+    off = torch.cat([torch.zeros(1, dtype=torch.int64, device=device), nl])
+    return b, off
 
 
 def _torch_bits(N: int, g, device):

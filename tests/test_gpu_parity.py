@@ -300,3 +300,23 @@ def test_full_size_sampled(rs, strategy):
             assert got[r] == ref, (dist, r)
         del vals, off, out, ws
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("strategy", ["signal", "tagged"])
+@pytest.mark.parametrize("line_mean,cls,base,chunk", [
+    (1397.0, b"{", 0, 8192), (1397.0, b"{", 7, 2048), (20.0, b"{0123456789", 13, 2048), (5000.0, b"", 3, 2048)])
+def test_text_count_xor64(rs, strategy, line_mean, cls, base, chunk):
+    """D4 shape: byte stream split on newlines, CLASS filter, COUNT + XOR64 of
+    mix64(i << 8 | byte) per line (reading A19) -- bit-exact; lines longer than
+    a chunk, unaligned starts (16-byte TMA blocks), and no filter at all (the
+    aggregate reads the byte ring directly)."""
+    b, off = synth.text(400000, seed=int(line_mean) + base, line_mean=line_mean)
+    if base:
+        b = np.concatenate([np.full(base, ord("x"), np.uint8), b])
+        off = off + base
+    stages = [("class", synth.class_table(cls))] if cls else []
+    ref = oracle.brute(b, off, stages, "count_xor64")
+    got, st, _ = run_gpu(rs, b, off, stages, "count_xor64", strategy, chunk=chunk)
+    got = [g.view(np.uint64) for g in got]
+    assert_parity(got, ref, "count_xor64")
+    assert st[0][2] == off[-1] - off[0]
