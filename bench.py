@@ -126,6 +126,10 @@ def workload_spec(name):
         return dict(N=1 << 29, dist=dist, L=int(l[1:]), stages=synth.sweep_stages(3), agg="sum_i64", dtype="i32")
     if name == "zipf":
         return dict(N=1 << 30, dist="zipf", L=0, stages=synth.sweep_stages(3), agg="sum_i64", dtype="i32")
+    if name == "graph":
+        return dict(N=16 << 24, dist="rmat", L=0, stages=[("lt_u32", 1 << 31)], agg="count_min_u32", dtype="u32")
+    if name == "text":
+        return dict(N=1 << 32, dist="text", L=0, stages=synth.text_stages(), agg="count_xor64", dtype="u8")
     raise ValueError(name)
 
 
@@ -133,6 +137,10 @@ def make_inputs(spec, seed, device):
     import synth
     import torch
     N, dist, L = spec["N"], spec["dist"], spec["L"]
+    if dist == "rmat":
+        return synth.torch_rmat_csr(24, 16, seed=seed, device=device)
+    if dist == "text":
+        return synth.torch_text(N, seed=seed, device=device)
     if dist == "fixed":
         lens = torch.full((N // L,), L, dtype=torch.int64, device=device)
     elif dist == "var":
@@ -146,8 +154,11 @@ def make_inputs(spec, seed, device):
 
 
 def alg_bytes(n, R, agg):
+    """Payload read once + offsets read once + one aggregate written per region
+    (SURVEY §8(d))."""
     out_b = {"sum_i64": 8, "sum_f32": 4, "count_min_u32": 8, "count_xor64": 16}[agg]
-    return 4 * n + 8 * (R + 1) + out_b * R
+    esz = 1 if agg == "count_xor64" else 4
+    return esz * n + 8 * (R + 1) + out_b * R
 
 
 # ------------------------------------------------------------------- oracle
@@ -280,9 +291,10 @@ def run_ours(args):
     p = rs.Pipeline(spec["stages"], spec["agg"], strategy=args.strategy, flags=flags)
     out = p.alloc_outputs(R, dev)
     ws = p.alloc_workspace(R, n, dev)
-    gather_buf = None
-    if world > 1 and rank == 0:
-        gather_buf = [torch.empty_like(out[0]) for _ in range(world)]
+    # weak scaling: rank k owns global regions [k*R, (k+1)*R) (whole regions,
+    # no exchange during the run); the aggregates are gathered to rank 0
+    from paper_2006_07478_b200.dist import gather_aggregates
+    bounds = [k * R for k in range(world + 1)]
 
     # ---- device-timed region: W warm-ups, then K steps, barrier + sync both sides
     stream = torch.cuda.current_stream()
@@ -302,7 +314,7 @@ def run_ours(args):
         for _ in range(args.steps):
             p.run(vals, off, out, ws)
             if world > 1:
-                dist.gather(out[0], gather_buf if rank == 0 else None, dst=0)
+                gather_aggregates(out[0], bounds, dst=0)
         t1.record(stream)
         torch.cuda.synchronize()
         clk.mark(w0, time.time())
@@ -361,9 +373,12 @@ def run_ours(args):
         rate, cores, desc = oracle_rate(vh, oh, spec["stages"], spec["agg"], budget_s=20.0)
         cpu = {"value": rate, "unit": "items/s", "cores": cores, "kind": "oracle", "sample": desc}
 
-    sweep = None
-    if args.sweep and rank == 0:
+    sweep = configs = None
+    if args.sweep and rank == 0 and world == 1:
+        del vals, off, out, ws
+        torch.cuda.empty_cache()
         sweep = run_sweep(rs, torch, dev, args)
+        configs = run_configs(rs, torch, dev, args)
 
     if rank == 0:
         line = {
@@ -386,9 +401,41 @@ def run_ours(args):
         }
         if sweep is not None:
             line["sweep"] = sweep
+        if configs is not None:
+            line["configs"] = configs
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_configs(rs, torch, dev, args):
+    """The other BASELINE configs on one GPU: R-MAT graph (D3), text lines (D4),
+    Zipf regions (D5, the 8-GPU config's 1-GPU point)."""
+    res = []
+    for name in ("graph", "text", "zipf"):
+        spec = workload_spec(name)
+        vals, off = make_inputs(spec, seed=0x5EED + 3, device=dev)
+        n, R = int(off[-1].item() - off[0].item()), off.numel() - 1
+        for strat in ("signal", "tagged"):
+            p = rs.Pipeline(spec["stages"], spec["agg"], strategy=strat, flags=rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING)
+            out = p.alloc_outputs(R, dev)
+            ws = p.alloc_workspace(R, vals.numel(), dev)
+            p.run(vals, off, out, ws)
+            torch.cuda.synchronize()
+            ms = []
+            for _ in range(args.sweep_reps):
+                p.run(vals, off, out, ws)
+                ms.append(sum(p.kernel_times()))
+            t = statistics.median(ms)
+            st = p.stats()
+            res.append({"workload": name, "strategy": strat, "children": n, "regions": R, "ms": t,
+                        "items_per_s": n / (t / 1e3),
+                        "hbm_frac": alg_bytes(n, R, spec["agg"]) / (t / 1e3) / 1e9 / hbm_peak()[0],
+                        "lane_fraction": [x["lane_fraction"] for x in lane_stats(st)], "error": p.check()})
+            del out, ws, p
+        del vals, off
+        torch.cuda.empty_cache()
+    return res
 
 
 def run_sweep(rs, torch, dev, args):

@@ -11,6 +11,9 @@ Workload recipes:
               int32 full range, 3 x HASH_LT(T=192), SUM_I64; fp32 variant
               U[0,1) with SUM_F32.  Fixed-children reading N = 2^29 (the
               paper's 512M integers).
+  D3 graph  : R-MAT scale 24 (Graph500 a,b,c,d = .57,.19,.19,.05, edge factor
+              16, random vertex relabel), edges grouped by source vertex (CSR),
+              u32 weights i.i.d. uniform; LT(2^31) filter, COUNT_MIN_U32.
   D4 text   : i.i.d. bytes: '\n' with p = 1/1397 (geometric lines of mean
               1397 chars), '{' with p = 45/1397 (~45 per line,
               P:681-682), digits with p = 1/2, other printable bytes
@@ -193,6 +196,30 @@ def torch_text(N: int, seed: int = 0, device="cuda", line_mean: float = 1397.0, 
         nl = torch.cat([nl, torch.tensor([N], dtype=torch.int64, device=device)])
     off = torch.cat([torch.zeros(1, dtype=torch.int64, device=device), nl])
     return b, off
+
+
+def torch_rmat_csr(scale: int = 24, edge_factor: int = 16, seed: int = 0, device="cuda",
+                   a: float = 0.57, b: float = 0.19, c: float = 0.19):
+    """D3: R-MAT source-vertex degrees -> CSR offsets (int64[V+1]) plus u32
+    edge weights (returned as an int32 view) per CSR slot.  Only the source of
+    each edge matters for grouping; its bit at every level is 1 with
+    probability c + d (the lower two quadrants), independently per level."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    V = 1 << scale
+    E = edge_factor * V
+    p1 = 1.0 - a - b                       # P(source bit = 1) = c + d
+    src = torch.zeros(E, dtype=torch.int64, device=device)
+    for lvl in range(scale):
+        bit = (torch.rand(E, generator=g, device=device) < p1).to(torch.int64)
+        src |= bit << lvl
+    perm = torch.randperm(V, generator=g, device=device)
+    deg = torch.bincount(perm[src], minlength=V)
+    del src
+    off = torch_offsets(deg)
+    w = _torch_bits(E, g, device).view(torch.int32)
+    return w, off
 
 
 def _torch_bits(N: int, g, device):

@@ -320,3 +320,18 @@ def test_text_count_xor64(rs, strategy, line_mean, cls, base, chunk):
     got = [g.view(np.uint64) for g in got]
     assert_parity(got, ref, "count_xor64")
     assert st[0][2] == off[-1] - off[0]
+
+
+@pytest.mark.parametrize("strategy", ["signal", "tagged"])
+def test_graph_rmat_count_min(rs, strategy):
+    """D3 shape: edges grouped by source vertex of an R-MAT graph (skewed
+    degrees: most vertices empty, a few with thousands of edges spanning
+    chunks), LT(2^31) weight filter, COUNT + MIN per vertex -- bit-exact."""
+    w, off = synth.torch_rmat_csr(16, 16, seed=5, device="cuda")
+    wv = w.cpu().numpy().view(np.uint32)
+    offh = off.cpu().numpy()
+    stages = [("lt_u32", 1 << 31)]
+    ref = oracle.brute(wv, offh, stages, "count_min_u32")
+    got, st, _ = run_gpu(rs, wv, offh, stages, "count_min_u32", strategy, chunk=2048)
+    assert_parity(got, ref, "count_min_u32")
+    assert (np.diff(offh) == 0).mean() > 0.3          # R-MAT: many isolated vertices
