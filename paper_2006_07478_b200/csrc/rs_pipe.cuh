@@ -129,6 +129,33 @@ __device__ __noinline__ uint32_t filter_batch(const uint32_t *in, const uint32_t
     return tl;
 }
 
+// One partial ensemble (e < w items: signal-bounded or the drained tail) of
+// a FILTER/TRANSFORM node; shared by every stage node (code size).
+template <bool TAG, bool U8IN>
+__device__ __noinline__ uint32_t partial_stage(const StageP *sp, const uint32_t *in, const uint32_t *tin,
+                                               uint32_t imask, uint32_t h, uint32_t e, uint32_t *out, uint32_t *tout,
+                                               uint32_t qmask, uint32_t tl, uint32_t lt, uint32_t cmask) {
+    const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll
+    for (int j = 0; j < IPL; ++j) {
+        const uint32_t idx = j * 32 + lane;
+        const bool act = idx < e;
+        uint32_t v = act ? load_item<U8IN>(in, h + idx, imask, cmask) : 0u;
+        uint32_t tg = 0;
+        if constexpr (TAG) tg = act ? tin[(h + idx) & imask] : 0u;
+        const bool keep = act && stage_apply(*sp, v);
+        const uint32_t mk = __ballot_sync(kFull, keep);   // stable compaction
+        if (keep) {
+            const uint32_t pos = (tl + __popc(mk & lt)) & qmask;
+            out[pos] = v;
+            if constexpr (TAG) tout[pos] = tg;
+        }
+        tl += __popc(mk);
+    }
+    __syncwarp();
+    return tl;
+}
+
 struct Chunk {
     int32_t k;             // chunk id (-1 = empty slot)
     long long beg, end;    // element range [beg, end)
@@ -738,29 +765,10 @@ struct Pipe {
                 agg_tagged(in, tin, imask, h, e);
             }
         } else {
-            const StageP &sp = P.st[n - 1];
-            uint32_t *out = Q<n>();
-            uint32_t *tout = T<n>();
-            uint32_t tl = E<n>().qt;
-#pragma unroll
-            for (int j = 0; j < IPL; ++j) {
-                const uint32_t idx = j * 32 + lane;
-                const bool act = idx < e;
-                uint32_t v = act ? load_item<U8 && n == 1>(in, h + idx, imask, P.C - 1) : 0u;
-                uint32_t tg = 0;
-                if constexpr (TAG) tg = act ? tin[(h + idx) & imask] : 0u;
-                const bool keep = act && stage_apply(sp, v);
-                const uint32_t mk = __ballot_sync(kFull, keep);   // stable compaction
-                if (keep) {
-                    const uint32_t pos = (tl + __popc(mk & lt)) & qmask;
-                    out[pos] = v;
-                    if constexpr (TAG) tout[pos] = tg;
-                }
-                tl += __popc(mk);
-            }
+            const uint32_t tl = partial_stage<TAG, U8 && n == 1>(&P.st[n - 1], in, tin, imask, h, e, Q<n>(), T<n>(),
+                                                                qmask, E<n>().qt, lt, P.C - 1);
             E<n>().sent += tl - E<n>().qt;
             E<n>().qt = tl;
-            __syncwarp();
         }
     }
 
