@@ -13,7 +13,8 @@ import os
 import struct
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "librs.so")
+# RS_LIB may point at another build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("RS_LIB") or os.path.join(_HERE, "lib", "librs.so")
 
 # rs.h enumerations (kept in sync with include/rs.h by tests/test_abi.py)
 RS_OK, RS_ERR_INVALID_ARG, RS_ERR_INVALID_TOPOLOGY, RS_ERR_UNSUPPORTED = 0, -1, -2, -3

@@ -693,7 +693,6 @@ struct Pipe {
                 run_full<n>(in, tin, imask, E<ei>().qh, nens);
                 E<ei>().qh += nens * W;
                 if (spend) E<ei>().cur -= nens * W;
-                stat_add(n, 1, nens);          // full ensembles (items/ensembles derived at exit)
                 prog = true;
                 continue;
             }
@@ -708,7 +707,8 @@ struct Pipe {
                 run_partial<n>(in, tin, imask, E<ei>().qh, e);
                 E<ei>().qh += e;
                 if (spend) E<ei>().cur -= e;
-                stat_add(n, 0, 1u);            // partial ensembles
+                stat_add(n, 0, 1u);            // partial ensembles and their items; full
+                stat_add(n, 1, e);             // ensembles are derived at exit
                 prog = true;
                 continue;
             }
@@ -853,9 +853,13 @@ struct Pipe {
     __device__ __forceinline__ void finish_counters() {
         if constexpr (n <= K + 1) {
             if (lane == 0) {
+                // c[0] = partial ensembles, c[1] = their items (accumulated in the run)
                 uint32_t *c = reinterpret_cast<uint32_t *>(base + 32) + 4 * n;
-                c[0] += c[1];
-                c[2] = E<n - 1>().qh - q_start[n - 1];
+                const uint32_t items = E<n - 1>().qh - q_start[n - 1];
+                const uint32_t full = (items - c[1]) / W;
+                c[0] += full;
+                c[1] = full;
+                c[2] = items;
                 c[3] = E<n - 1>().sh;                      // signals consumed
                 if constexpr (n == 1) {                     // enumerate: items / signals emitted
                     c[-4 + 2] = E<0>().qt - q_start[0];
