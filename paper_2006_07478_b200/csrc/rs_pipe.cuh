@@ -59,61 +59,30 @@ template <bool TAG, int NS, class Op, bool U8IN>
 __device__ __forceinline__ void filter_slices(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                               uint32_t *out, uint32_t *tout, uint32_t qmask, uint32_t &tl,
                                               const Op &op, uint32_t lt, uint32_t cmask) {
+    // Masked ring addressing only (no wrap-free fast path): the smaller code
+    // measured faster than the dual-path variant (tools/ab.py, profiles/).
     const uint32_t lane = threadIdx.x & 31u;
     uint32_t v[NS], tg[NS];
     bool keep[NS];
-    if (((h & imask) + NS * 32) <= imask + 1) {        // input range does not wrap the ring
-        if constexpr (U8IN) {
-            const uint8_t *src8 = reinterpret_cast<const uint8_t *>(in) + (h & imask) + lane;
 #pragma unroll
-            for (int j = 0; j < NS; ++j) v[j] = (uint32_t)src8[32 * j] | (((h + 32 * j + lane) & cmask) << 8);
-        } else {
-            const uint32_t *src = in + (h & imask) + lane;
+    for (int j = 0; j < NS; ++j) v[j] = load_item<U8IN>(in, h + 32 * j + lane, imask, cmask);
+    if constexpr (TAG) {
 #pragma unroll
-            for (int j = 0; j < NS; ++j) v[j] = src[32 * j];
-        }
-        if constexpr (TAG) {
-            const uint32_t *ts = tin + (h & imask) + lane;
-#pragma unroll
-            for (int j = 0; j < NS; ++j) tg[j] = ts[32 * j];
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < NS; ++j) v[j] = load_item<U8IN>(in, h + 32 * j + lane, imask, cmask);
-        if constexpr (TAG) {
-#pragma unroll
-            for (int j = 0; j < NS; ++j) tg[j] = tin[(h + 32 * j + lane) & imask];
-        }
+        for (int j = 0; j < NS; ++j) tg[j] = tin[(h + 32 * j + lane) & imask];
     }
 #pragma unroll
     for (int j = 0; j < NS; ++j) keep[j] = op(v[j]);
     uint32_t mk[NS];
 #pragma unroll
     for (int j = 0; j < NS; ++j) mk[j] = __ballot_sync(kFull, keep[j]);
-    if (((tl & qmask) + NS * 32) <= qmask + 1) {        // output range does not wrap the ring
-        uint32_t *dst = out + (tl & qmask);
-        uint32_t *tdst = TAG ? tout + (tl & qmask) : nullptr;
-        uint32_t off = 0;
 #pragma unroll
-        for (int j = 0; j < NS; ++j) {
-            if (keep[j]) {
-                const uint32_t o = off + __popc(mk[j] & lt);
-                dst[o] = v[j];
-                if constexpr (TAG) tdst[o] = tg[j];
-            }
-            off += __popc(mk[j]);
+    for (int j = 0; j < NS; ++j) {
+        if (keep[j]) {
+            const uint32_t pos = (tl + __popc(mk[j] & lt)) & qmask;
+            out[pos] = v[j];
+            if constexpr (TAG) tout[pos] = tg[j];
         }
-        tl += off;
-    } else {
-#pragma unroll
-        for (int j = 0; j < NS; ++j) {
-            if (keep[j]) {
-                const uint32_t pos = (tl + __popc(mk[j] & lt)) & qmask;
-                out[pos] = v[j];
-                if constexpr (TAG) tout[pos] = tg[j];
-            }
-            tl += __popc(mk[j]);
-        }
+        tl += __popc(mk[j]);
     }
 }
 
@@ -122,9 +91,7 @@ __device__ __noinline__ uint32_t filter_batch(const uint32_t *in, const uint32_t
                                               uint32_t nens, uint32_t *out, uint32_t *tout, uint32_t qmask,
                                               uint32_t tl, const Op op, uint32_t lt, uint32_t cmask = 0) {
     uint32_t k = 0;
-    for (; k + 2 <= nens; k += 2, h += 2 * W)
-        filter_slices<TAG, 2 * IPL, Op, U8IN>(in, tin, imask, h, out, tout, qmask, tl, op, lt, cmask);
-    if (k < nens) filter_slices<TAG, IPL, Op, U8IN>(in, tin, imask, h, out, tout, qmask, tl, op, lt, cmask);
+    for (; k < nens; ++k, h += W) filter_slices<TAG, IPL, Op, U8IN>(in, tin, imask, h, out, tout, qmask, tl, op, lt, cmask);
     __syncwarp();
     return tl;
 }
