@@ -1,31 +1,9 @@
-// rs.cu — B200 (sm_100a) persistent pipeline kernels + the C ABI of include/rs.h.
+// rs.cu — the C ABI of include/rs.h (host side of the B200 pipeline).
 //
-// Hot path of Timcheck & Buhler, arXiv 2006.07478 (PAPER.md line refs "P:a-b").
-//
-// Execution model (§2.2, re-designed for B200):
-//  * One pipeline INSTANCE per warp.  An ensemble holds up to w = 128 items
-//    (4 per lane, item t of an ensemble lives in lane t%32, slot t/32), the
-//    paper's SIMD width.  All scheduler state is warp-uniform.
-//  * Instances compete for one parent stream with atomics: the
-//    stream is cut into child-balanced CHUNKS of C children whose first region
-//    is found by a prepass; an instance claims chunk k with atomicAdd.
-//    Regions crossing a chunk boundary are split into parts whose partial
-//    aggregates are combined by a fixup kernel (commutative monoids, A18).
-//  * Nodes: 0 = ENUMERATE, 1..K = FILTER/TRANSFORM, K+1 = AGGREGATE, joined
-//    by fixed-size shared-memory queues and, for the signal
-//    strategy, parallel signal queues.  Queue Q0 (enumerate ->
-//    first stage) is a TMA-fed ring: element blocks are bulk-copied from HBM
-//    (cp.async.bulk + mbarrier) ahead of the enumerate node's emission.
-//  * Scheduler: each sweep visits nodes upstream -> downstream and lets each
-//    fire repeatedly (data phase, then signal phase) under the
-//    full-first policy (A8): ensembles are full, or bounded by a
-//    pending signal's credit, or the upstream is drained.
-//  * Credit protocol exactly as P:304-327: sender rule (1)/(2) with an
-//    emitted-since-last-signal counter; receiver counter with transfer (2b).
-#include "../../include/rs.h"
-#include "rs_device.cuh"
-
-#include <cuda_runtime.h>
+// Kernels live in rs_kern.cuh / rs_pipe.cuh / rs_ws.cuh and are instantiated per
+// aggregate in rs_k<AGG>.cu; see rs_kern.cuh for the execution model.
+#define RS_HOST_ONLY
+#include "rs_kern.cuh"
 
 #include <algorithm>
 #include <cstdio>
@@ -33,154 +11,9 @@
 #include <mutex>
 #include <string>
 
-using namespace rs;
+using namespace rsk;
 
 namespace {
-
-constexpr int W = 128;              // ensemble capacity (items)
-constexpr int IPL = W / 32;         // items per lane per ensemble
-constexpr uint32_t SLOT = 0x80000000u;  // key bit: partial-aggregate slot instead of region id
-constexpr uint32_t END_BIT = 0x80000000u;  // signal word: kind End
-constexpr int MAXK = 4;             // max FILTER/TRANSFORM stages
-constexpr int NST = 4;              // TMA stages in the Q0 ring
-constexpr int WPB = 4;              // warps (instances) per CTA
-
-enum : int32_t { ERR_OFFSETS = 1, ERR_WATCHDOG = 2, ERR_SIGFULL = 3, ERR_UNMATCHED = 4, ERR_QFULL = 5, ERR_LIMIT = 7 };
-
-struct StageP {
-    int32_t kind, op;
-    uint32_t a, b;
-    uint32_t table[8];
-};
-
-// Workspace header (first 64 bytes of the workspace).
-struct WsHdr {
-    uint32_t claim;      // parent-stream cursor (chunks)
-    int32_t err;         // first device error
-    uint32_t nchunks;
-    uint32_t pad_;
-    long long base0;     // align_down(offsets[0], 16 bytes)
-    long long off0, offR;
-};
-
-struct KParams {
-    const uint8_t *elems;
-    long long n_elems;
-    const long long *off;
-    long long R;
-    void *out0, *out1;
-    void *part0, *part1;            // partial slots [2 * max_chunks]
-    WsHdr *hdr;
-    uint32_t *chunk_fr;             // first region of chunk k, [max_chunks + 1]
-    unsigned long long *stats;      // [(K+2) * 4]
-    long long max_chunks;
-    uint32_t C;                     // chunk length (children)
-    uint32_t qcap, scap;            // queue / signal capacities (powers of 2)
-    uint32_t q0_stage;              // Q0 TMA stage size in elements (sequential kernel)
-    uint32_t esize;                 // element size in bytes (1 = u8 text, else 4)
-    uint32_t flags;
-    int32_t tagged;
-    int32_t nst;
-    StageP st[MAXK];
-};
-
-// ------------------------------------------------------------ stage ops
-// isGood() / push() bodies (Fig. 5); readings A13/A14.
-__device__ __forceinline__ bool stage_apply(const StageP &s, uint32_t &v) {
-    switch (s.op) {
-        case RS_OP_HASH_LT: return ((v * s.a) >> 24) < s.b;
-        case RS_OP_LT_U32: return s.table[0] ? true : v < s.b;    // table[0]: bound == 2^32
-        case RS_OP_CLASS: return (s.table[(v & 0xffu) >> 5] >> (v & 31u)) & 1u;
-        case RS_OP_SCALE_F32: v = __float_as_uint(__fmul_rn(__uint_as_float(s.a), __uint_as_float(v))); return true;
-        case RS_OP_AFFINE_I32: v = v * s.a + s.b; return true;
-    }
-    return true;
-}
-
-// --------------------------------------------------------------- prepass
-// Chunk boundaries: b_0 = off0, b_k = base0 + k*C; chunk_fr[k] = first region
-// r with off[r] >= b_k (lower bound over off[0..R-1]); chunk_fr[nchunks] = R.
-// Also resets the claim counter / error word / stats, initialises partial
-// slots to the identity and (tagged strategy) the outputs to the identity
-// (A1: regions none of whose items reach the aggregate report identity).
-template <int AGG>
-__global__ void k_prepass(KParams P, int n_stats) {
-    using AT = AggT<AGG>;
-    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long nth = (long long)gridDim.x * blockDim.x;
-    const long long off0 = P.off[0], offR = P.off[P.R];
-    const long long align = 16;  // bytes: TMA copies whole 16-byte blocks
-    const long long esz = P.esize;
-    const long long base0 = (off0 * esz / align) * align / esz;
-    long long span = offR - base0;
-    long long nch = span <= 0 ? 1 : (span + P.C - 1) / P.C;
-    bool bad = nch > P.max_chunks || offR < off0 || off0 < 0 || offR > P.n_elems;
-    if (bad) nch = 0;
-    if (tid == 0) {
-        P.hdr->claim = 0;
-        P.hdr->err = bad ? ERR_OFFSETS : 0;
-        P.hdr->nchunks = (uint32_t)nch;
-        P.hdr->base0 = base0;
-        P.hdr->off0 = off0;
-        P.hdr->offR = offR;
-    }
-    for (long long i = tid; i < n_stats; i += nth) P.stats[i] = 0ull;
-    for (long long k = tid; k <= nch; k += nth) {
-        uint32_t fr;
-        if (k == nch) {
-            fr = (uint32_t)P.R;
-        } else {
-            long long b = (k == 0) ? off0 : base0 + k * (long long)P.C;
-            long long lo = 0, hi = P.R;  // first r in [0,R) with off[r] >= b, else R
-            while (lo < hi) {
-                long long mid = (lo + hi) >> 1;
-                if (P.off[mid] < b) lo = mid + 1; else hi = mid;
-            }
-            fr = (uint32_t)lo;
-        }
-        P.chunk_fr[k] = fr;
-    }
-    for (long long s = tid; s < 2 * nch; s += nth) AT::store(P.part0, P.part1, (uint64_t)s, AT::id());
-    if (P.tagged)
-        for (long long r = tid; r < P.R; r += nth) AT::store(P.out0, P.out1, (uint64_t)r, AT::id());
-    if (P.flags & RS_FLAG_VALIDATE) {
-        for (long long r = tid; r < P.R; r += nth)
-            if (P.off[r + 1] < P.off[r]) atomicCAS((int *)&P.hdr->err, 0, ERR_OFFSETS);
-        if (tid == 0 && (offR > P.n_elems || off0 < 0)) atomicCAS((int *)&P.hdr->err, 0, ERR_OFFSETS);
-    }
-}
-
-// ----------------------------------------------------------------- fixup
-// Combine the partial aggregates of regions split across chunks (A18): the
-// chunk whose tail part starts region r walks forward over the head parts.
-template <int AGG>
-__global__ void k_fixup(KParams P) {
-    using AT = AggT<AGG>;
-    const WsHdr *H = P.hdr;
-    const long long nch = H->nchunks;
-    const long long base0 = H->base0, offR = H->offR;
-    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k + 1 < nch;
-         k += (long long)gridDim.x * blockDim.x) {
-        uint32_t f0 = P.chunk_fr[k], f1 = P.chunk_fr[k + 1];
-        if (f1 <= f0) continue;                       // no region starts in chunk k
-        long long r = (long long)f1 - 1;               // last region starting in chunk k
-        long long end_k = base0 + (k + 1) * (long long)P.C;
-        long long rend = P.off[r + 1];
-        if (rend <= end_k) continue;                   // not split
-        typename AT::A acc = AT::load(P.part0, P.part1, (uint64_t)(2 * k + 1));
-        for (long long j = k + 1; j < nch; ++j) {
-            acc = AT::comb(acc, AT::load(P.part0, P.part1, (uint64_t)(2 * j)));
-            long long end_j = base0 + (j + 1) * (long long)P.C;
-            if (end_j > offR) end_j = offR;
-            if (rend <= end_j) break;
-        }
-        AT::store(P.out0, P.out1, (uint64_t)r, acc);
-    }
-}
-
-// ---------------------------------------------------------- the pipeline
-#include "rs_pipe.cuh"
-#include "rs_ws.cuh"
 
 // ------------------------------------------------------------ host side
 thread_local std::string g_err;
@@ -215,82 +48,12 @@ struct rs_pipeline {
 
 namespace {
 
-using KernelFn = void (*)(KParams);
-
-template <int AGG, bool TAG>
-KernelFn pick_k(int K) {
-    switch (K) {
-        case 0: return k_pipeline<0, AGG, TAG>;
-        case 1: return k_pipeline<1, AGG, TAG>;
-        case 2: return k_pipeline<2, AGG, TAG>;
-        case 3: return k_pipeline<3, AGG, TAG>;
-        default: return k_pipeline<4, AGG, TAG>;
-    }
-}
-
-template <int AGG, bool TAG>
-KernelFn pick_ws(int K) {
-    switch (K) {
-        case 0: return k_pipeline_ws<0, AGG, TAG>;
-        case 1: return k_pipeline_ws<1, AGG, TAG>;
-        case 2: return k_pipeline_ws<2, AGG, TAG>;
-        case 3: return k_pipeline_ws<3, AGG, TAG>;
-        default: return k_pipeline_ws<4, AGG, TAG>;
-    }
-}
-
-template <int AGG, bool TAG>
-uint32_t smem_ws(int K, uint32_t qcap, uint32_t scap) {
-    switch (K) {
-        case 0: return WS<0, AGG, TAG>::smem_bytes(qcap, scap);
-        case 1: return WS<1, AGG, TAG>::smem_bytes(qcap, scap);
-        case 2: return WS<2, AGG, TAG>::smem_bytes(qcap, scap);
-        case 3: return WS<3, AGG, TAG>::smem_bytes(qcap, scap);
-        default: return WS<4, AGG, TAG>::smem_bytes(qcap, scap);
-    }
-}
-
-template <int AGG, bool TAG>
-uint32_t smem_for(int K, uint32_t qcap, uint32_t scap, uint32_t sblk) {
-    switch (K) {
-        case 0: return Pipe<0, AGG, TAG>::smem_bytes(qcap, scap, sblk);
-        case 1: return Pipe<1, AGG, TAG>::smem_bytes(qcap, scap, sblk);
-        case 2: return Pipe<2, AGG, TAG>::smem_bytes(qcap, scap, sblk);
-        case 3: return Pipe<3, AGG, TAG>::smem_bytes(qcap, scap, sblk);
-        default: return Pipe<4, AGG, TAG>::smem_bytes(qcap, scap, sblk);
-    }
-}
-
-struct Launch {
-    KernelFn main;
-    KernelFn ws;
-    uint32_t ws_bytes;
-    void (*pre)(KParams, int);
-    void (*fix)(KParams);
-    uint32_t inst_bytes;
-    int out_bytes0, out_bytes1;
-};
-
-template <int AGG>
-Launch launch_for(int K, bool tag, uint32_t qcap, uint32_t scap, uint32_t sblk) {
-    Launch L;
-    L.main = tag ? pick_k<AGG, true>(K) : pick_k<AGG, false>(K);
-    L.ws = tag ? pick_ws<AGG, true>(K) : pick_ws<AGG, false>(K);
-    L.ws_bytes = tag ? smem_ws<AGG, true>(K, qcap, scap) : smem_ws<AGG, false>(K, qcap, scap);
-    L.pre = k_prepass<AGG>;
-    L.fix = k_fixup<AGG>;
-    L.inst_bytes = tag ? smem_for<AGG, true>(K, qcap, scap, sblk) : smem_for<AGG, false>(K, qcap, scap, sblk);
-    L.out_bytes0 = AggT<AGG>::bytes0;
-    L.out_bytes1 = AggT<AGG>::bytes1;
-    return L;
-}
-
 bool get_launch(const rs_pipeline *p, Launch *L) {
     switch (p->agg) {
-        case RS_OP_SUM_I64: *L = launch_for<20>(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
-        case RS_OP_SUM_F32: *L = launch_for<21>(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
-        case RS_OP_COUNT_MIN_U32: *L = launch_for<22>(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
-        case RS_OP_COUNT_XOR64: *L = launch_for<23>(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
+        case RS_OP_SUM_I64: *L = launch_agg20(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
+        case RS_OP_SUM_F32: *L = launch_agg21(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
+        case RS_OP_COUNT_MIN_U32: *L = launch_agg22(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
+        case RS_OP_COUNT_XOR64: *L = launch_agg23(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
     }
     return false;
 }

@@ -1,0 +1,8 @@
+// rs_k20.cu — kernel instantiations for aggregate op 20 (see rs_kern.cuh).
+#include "rs_kern.cuh"
+
+namespace rsk {
+Launch launch_agg20(int K, bool tag, uint32_t qcap, uint32_t scap, uint32_t sblk) {
+    return launch_for<20>(K, tag, qcap, scap, sblk);
+}
+}  // namespace rsk

@@ -1,0 +1,8 @@
+// rs_k22.cu — kernel instantiations for aggregate op 22 (see rs_kern.cuh).
+#include "rs_kern.cuh"
+
+namespace rsk {
+Launch launch_agg22(int K, bool tag, uint32_t qcap, uint32_t scap, uint32_t sblk) {
+    return launch_for<22>(K, tag, qcap, scap, sblk);
+}
+}  // namespace rsk

@@ -36,3 +36,12 @@ tot = sum(agg.values()); tots = sum(stl.values()) or 1
 print(f"total executed {tot}, mapped {sum(v for k, v in agg.items() if k)}")
 for k, v in agg.most_common(45):
     print(f"{100*v/tot:5.1f}%  stalls {100*stl[k]/tots:5.1f}%  {k}")
+if len(sys.argv) > 4:
+    # coarse grouping by source ranges: "file:lo-hi=name,..."
+    for spec in sys.argv[4].split(","):
+        rng, name = spec.split("=")
+        f, lh = rng.split(":")
+        lo, hi = map(int, lh.split("-"))
+        v = sum(n for k, n in agg.items() if k and k[0] == f and lo <= k[1] <= hi)
+        s = sum(n for k, n in stl.items() if k and k[0] == f and lo <= k[1] <= hi)
+        print(f"{name:>12}: inst {100*v/tot:5.1f}%  stalls {100*s/tots:5.1f}%")
