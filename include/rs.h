@@ -98,10 +98,17 @@ enum {
     RS_FLAG_VALIDATE = 2u,   /* device-check offsets monotone and <= n_elems          */
     RS_FLAG_TIMING = 4u,     /* record CUDA events around each kernel of a run        */
     RS_FLAG_PROFILE = 16u,   /* per-node clock64() cycle counters (rs_pipeline_profile)  */
-    RS_FLAG_WARP_SPECIALIZED = 8u  /* one CTA per instance with one warp per node, nodes
+    RS_FLAG_WARP_SPECIALIZED = 8u, /* one CTA per instance with one warp per node, nodes
                                       running concurrently (signals carry emission positions),
                                       instead of the default one-warp instance whose scheduler
                                       fires one node at a time */
+    RS_FLAG_UNFUSED = 32u    /* sequential scheduler: keep the AGGREGATE as a separate node
+                                with its own queue (the paper's node structure).
+                                Default: the aggregate is folded into the last FILTER/
+                                TRANSFORM node, which adds its surviving items straight into
+                                the per-region accumulator (same results; the AGGREGATE's
+                                stats then report that node's firings).  No effect with
+                                RS_FLAG_WARP_SPECIALIZED or without stages. */
 };
 
 typedef struct {

@@ -50,10 +50,10 @@ namespace {
 
 bool get_launch(const rs_pipeline *p, Launch *L) {
     switch (p->agg) {
-        case RS_OP_SUM_I64: *L = launch_agg20(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
-        case RS_OP_SUM_F32: *L = launch_agg21(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
-        case RS_OP_COUNT_MIN_U32: *L = launch_agg22(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
-        case RS_OP_COUNT_XOR64: *L = launch_agg23(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
+        case RS_OP_SUM_I64: *L = launch_agg20(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
+        case RS_OP_SUM_F32: *L = launch_agg21(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
+        case RS_OP_COUNT_MIN_U32: *L = launch_agg22(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
+        case RS_OP_COUNT_XOR64: *L = launch_agg23(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
     }
     return false;
 }

@@ -194,20 +194,20 @@ struct Launch {
 };
 
 // One per aggregate, defined in rs_k<AGG>.cu.
-Launch launch_agg20(int K, bool tag, uint32_t qcap, uint32_t scap, uint32_t sblk);
-Launch launch_agg21(int K, bool tag, uint32_t qcap, uint32_t scap, uint32_t sblk);
-Launch launch_agg22(int K, bool tag, uint32_t qcap, uint32_t scap, uint32_t sblk);
-Launch launch_agg23(int K, bool tag, uint32_t qcap, uint32_t scap, uint32_t sblk);
+Launch launch_agg20(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk);
+Launch launch_agg21(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk);
+Launch launch_agg22(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk);
+Launch launch_agg23(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk);
 
 #ifndef RS_HOST_ONLY
-template <int AGG, bool TAG>
+template <int AGG, bool TAG, bool FUSE>
 KernelFn pick_k(int K) {
     switch (K) {
-        case 0: return k_pipeline<0, AGG, TAG>;
-        case 1: return k_pipeline<1, AGG, TAG>;
-        case 2: return k_pipeline<2, AGG, TAG>;
-        case 3: return k_pipeline<3, AGG, TAG>;
-        default: return k_pipeline<4, AGG, TAG>;
+        case 0: return k_pipeline<0, AGG, TAG, false>;      // nothing to fuse
+        case 1: return k_pipeline<1, AGG, TAG, FUSE>;
+        case 2: return k_pipeline<2, AGG, TAG, FUSE>;
+        case 3: return k_pipeline<3, AGG, TAG, FUSE>;
+        default: return k_pipeline<4, AGG, TAG, FUSE>;
     }
 }
 
@@ -233,27 +233,29 @@ uint32_t smem_ws(int K, uint32_t qcap, uint32_t scap) {
     }
 }
 
-template <int AGG, bool TAG>
+template <int AGG, bool TAG, bool FUSE>
 uint32_t smem_for(int K, uint32_t qcap, uint32_t scap, uint32_t sblk) {
     switch (K) {
-        case 0: return Pipe<0, AGG, TAG>::smem_bytes(qcap, scap, sblk);
-        case 1: return Pipe<1, AGG, TAG>::smem_bytes(qcap, scap, sblk);
-        case 2: return Pipe<2, AGG, TAG>::smem_bytes(qcap, scap, sblk);
-        case 3: return Pipe<3, AGG, TAG>::smem_bytes(qcap, scap, sblk);
-        default: return Pipe<4, AGG, TAG>::smem_bytes(qcap, scap, sblk);
+        case 0: return Pipe<0, AGG, TAG, false>::smem_bytes(qcap, scap, sblk);
+        case 1: return Pipe<1, AGG, TAG, FUSE>::smem_bytes(qcap, scap, sblk);
+        case 2: return Pipe<2, AGG, TAG, FUSE>::smem_bytes(qcap, scap, sblk);
+        case 3: return Pipe<3, AGG, TAG, FUSE>::smem_bytes(qcap, scap, sblk);
+        default: return Pipe<4, AGG, TAG, FUSE>::smem_bytes(qcap, scap, sblk);
     }
 }
 
 
 template <int AGG>
-Launch launch_for(int K, bool tag, uint32_t qcap, uint32_t scap, uint32_t sblk) {
+Launch launch_for(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk) {
     Launch L;
-    L.main = tag ? pick_k<AGG, true>(K) : pick_k<AGG, false>(K);
+    L.main = tag ? (fuse ? pick_k<AGG, true, true>(K) : pick_k<AGG, true, false>(K))
+                 : (fuse ? pick_k<AGG, false, true>(K) : pick_k<AGG, false, false>(K));
     L.ws = tag ? pick_ws<AGG, true>(K) : pick_ws<AGG, false>(K);
     L.ws_bytes = tag ? smem_ws<AGG, true>(K, qcap, scap) : smem_ws<AGG, false>(K, qcap, scap);
     L.pre = k_prepass<AGG>;
     L.fix = k_fixup<AGG>;
-    L.inst_bytes = tag ? smem_for<AGG, true>(K, qcap, scap, sblk) : smem_for<AGG, false>(K, qcap, scap, sblk);
+    L.inst_bytes = tag ? (fuse ? smem_for<AGG, true, true>(K, qcap, scap, sblk) : smem_for<AGG, true, false>(K, qcap, scap, sblk))
+                       : (fuse ? smem_for<AGG, false, true>(K, qcap, scap, sblk) : smem_for<AGG, false, false>(K, qcap, scap, sblk));
     L.out_bytes0 = AggT<AGG>::bytes0;
     L.out_bytes1 = AggT<AGG>::bytes1;
     return L;

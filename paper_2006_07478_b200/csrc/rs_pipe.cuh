@@ -40,6 +40,11 @@ struct OpAffine {
     }
 };
 
+struct OpDyn {             // runtime op (partial ensembles)
+    const StageP *s;
+    __device__ __forceinline__ bool operator()(uint32_t &v) const { return stage_apply(*s, v); }
+};
+
 // Full ensembles of a FILTER/TRANSFORM node, specialised per op and shared
 // by every stage node (one copy of the code keeps the hot loop inside the
 // instruction cache).  Item t of an ensemble lives in lane t%32, slot t/32.
@@ -131,10 +136,22 @@ struct Chunk {
     bool head;             // chunk starts inside region fr0-1 (a head part)
 };
 
-template <int K, int AGG, bool TAG>
+// FUSE: the AGGREGATE node is folded into the last FILTER/TRANSFORM node
+// (DESIGN.md §5 "fused terminal aggregate"): node K applies its op and adds
+// the surviving items of each ensemble straight into the accumulator and
+// performs the aggregate's Begin/End actions for the signals it consumes --
+// no compaction into, and no re-read of, a final queue.  The aggregate is a
+// commutative per-region fold and the signal strategy keeps every ensemble
+// inside one region, so the result is the same as with a separate node (the
+// tagged strategy folds by key as before).  FUSE=false is the paper's node
+// structure, kept for RS_FLAG_UNFUSED.
+template <int K, int AGG, bool TAG, bool FUSE>
 struct Pipe {
     using AT = AggT<AGG>;
     using A = typename AT::A;
+    static constexpr bool NA = FUSE && K >= 1;        // aggregate fused into node K
+    static constexpr int NQ = NA ? K - 1 : K;         // shared-memory data queues Q_1..Q_NQ
+    static constexpr int NSG = NA ? K : K + 1;        // signal rings S_0..S_{NSG-1}
     static constexpr uint32_t default_stage() { return TAG ? 256u : 512u; }
     static constexpr bool U8 = (AGG == 23);          // text stream: byte elements
     static constexpr uint32_t ESZ = U8 ? 1u : 4u;    // element size in the Q0 ring (bytes)
@@ -192,7 +209,7 @@ struct Pipe {
         else return Q<e>() + qcap;
     }
     template <int e> __device__ __forceinline__ uint2 *S() const {
-        return reinterpret_cast<uint2 *>(base + HDR + q0_bytes(sblk) + (TAG ? ring0 * 4 : 0) + K * qcap * 4 * (TAG ? 2 : 1)) +
+        return reinterpret_cast<uint2 *>(base + HDR + q0_bytes(sblk) + (TAG ? ring0 * 4 : 0) + NQ * qcap * 4 * (TAG ? 2 : 1)) +
                e * scap;
     }
 
@@ -212,6 +229,7 @@ struct Pipe {
     A carry;           // tagged: uniform partial of the carry region
     long long adelta;  // text aggregate: index offset of the current part (see part_delta)
     uint32_t dkey;     // tagged text aggregate: key whose delta is cached in adelta (per lane)
+    uint32_t fkept;    // fused aggregate: items that reached it (per lane; node statistics)
     long long base0, offR, off0;
     uint32_t nchunks;
     uint32_t q_start[K + 1];       // initial queue positions (edge 0 may start at the chunk-0 pad)
@@ -247,6 +265,7 @@ struct Pipe {
         akey = 0xffffffffu;
         adelta = 0;
         dkey = 0xffffffffu;
+        fkept = 0;
         base0 = P.hdr->base0;
         offR = P.hdr->offR;
         off0 = P.hdr->off0;
@@ -254,8 +273,8 @@ struct Pipe {
     }
 
     __host__ __device__ static constexpr uint32_t smem_bytes(uint32_t qcap, uint32_t scap, uint32_t sblk) {
-        return HDR + q0_bytes(sblk) + (TAG ? NST * sblk * 4 : 0) + K * qcap * 4 * (TAG ? 2 : 1) +
-               (TAG ? 0 : (K + 1) * scap * 8);
+        return HDR + q0_bytes(sblk) + (TAG ? NST * sblk * 4 : 0) + NQ * qcap * 4 * (TAG ? 2 : 1) +
+               (TAG ? 0 : NSG * scap * 8);
     }
 
     // ---------------------------------------------------------- chunks
@@ -557,7 +576,7 @@ struct Pipe {
         E<n>().qt = tl;
     }
 
-    static constexpr bool AGG_U8IN = U8 && K == 0;     // aggregate reads the byte ring directly
+    static constexpr bool AGG_U8IN = U8 && (NA ? K == 1 : K == 0);   // aggregate reads the byte ring directly
     __device__ __forceinline__ uint32_t agg_load(const uint32_t *in, uint32_t pos, uint32_t imask) const {
         return load_item<AGG_U8IN>(in, pos, imask, P.C - 1);
     }
@@ -601,6 +620,31 @@ struct Pipe {
         if (k < nens) agg_slices<IPL>(in, imask, h);
     }
 
+    // Fused node K, full ensembles (signal strategy): apply the op, fold the
+    // survivors into the per-lane accumulator (isGood + a::run).
+    template <class Op>
+    __device__ __forceinline__ void fused_full(const uint32_t *in, uint32_t imask, uint32_t h, uint32_t nens, const Op op) {
+        for (uint32_t k = 0; k < nens; ++k, h += W) {
+            uint32_t v[IPL];
+#pragma unroll
+            for (int j = 0; j < IPL; ++j) v[j] = agg_load(in, h + 32 * j + lane, imask);
+            A part = AT::id();
+#pragma unroll
+            for (int j = 0; j < IPL; ++j) {
+                const bool keep = op(v[j]);
+                fkept += keep ? 1u : 0u;
+                if (keep) part = AT::comb(part, AT::lift_i(v[j], adelta));
+            }
+            acc = AT::comb(acc, part);
+        }
+    }
+    template <class Op>
+    __device__ __forceinline__ void fused_run(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
+                                              uint32_t nens, const Op op) {
+        if constexpr (!TAG) fused_full(in, imask, h, nens, op);
+        else for (uint32_t k = 0; k < nens; ++k) agg_tagged(in, tin, imask, h + k * W, W, op);
+    }
+
     template <int n>
     __device__ __forceinline__ void run_full(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                              uint32_t nens) {
@@ -608,7 +652,22 @@ struct Pipe {
             if constexpr (!TAG) {
                 agg_full(in, imask, h, nens);
             } else {
-                for (uint32_t k = 0; k < nens; ++k) agg_tagged(in, tin, imask, h + k * W, W);
+                for (uint32_t k = 0; k < nens; ++k) agg_tagged(in, tin, imask, h + k * W, W, OpAll{});
+            }
+        } else if constexpr (NA && n == K) {
+            const StageP &sp = P.st[n - 1];
+            switch (sp.op) {
+                case RS_OP_HASH_LT:
+                    if (sp.b >= 256) fused_run(in, tin, imask, h, nens, OpAll{});
+                    else fused_run(in, tin, imask, h, nens, OpHash{sp.a, sp.b << 24});
+                    break;
+                case RS_OP_LT_U32:
+                    if (sp.table[0]) fused_run(in, tin, imask, h, nens, OpAll{});
+                    else fused_run(in, tin, imask, h, nens, OpLt{sp.b, false});
+                    break;
+                case RS_OP_CLASS: fused_run(in, tin, imask, h, nens, OpClass{sp.table}); break;
+                case RS_OP_SCALE_F32: fused_run(in, tin, imask, h, nens, OpScale{__uint_as_float(sp.a)}); break;
+                default: fused_run(in, tin, imask, h, nens, OpAffine{sp.a, sp.b}); break;
             }
         } else {
             const StageP &sp = P.st[n - 1];
@@ -634,7 +693,7 @@ struct Pipe {
     template <int n>
     __device__ __forceinline__ bool fire(bool drained) {
         constexpr int ei = n - 1;          // input edge
-        constexpr bool AGGN = (n == K + 1);
+        constexpr bool AGGN = (n == K + 1) || (NA && n == K);   // node n performs the aggregate's actions
         const uint32_t imask = (ei == 0) ? (ring0 - 1) : qmask;
         const uint32_t *in = Q<ei>();
         const uint32_t *tin = T<ei>();
@@ -729,7 +788,21 @@ struct Pipe {
                     if (idx < e) acc = AT::comb(acc, AT::lift_i(agg_load(in, h + idx, imask), adelta));
                 }
             } else {
-                agg_tagged(in, tin, imask, h, e);
+                agg_tagged(in, tin, imask, h, e, OpAll{});
+            }
+        } else if constexpr (NA && n == K) {
+            if constexpr (!TAG) {
+                const OpDyn op{&P.st[n - 1]};
+#pragma unroll
+                for (int j = 0; j < IPL; ++j) {
+                    const uint32_t idx = j * 32 + lane;
+                    uint32_t v = idx < e ? agg_load(in, h + idx, imask) : 0u;
+                    const bool keep = idx < e && op(v);
+                    fkept += keep ? 1u : 0u;
+                    if (keep) acc = AT::comb(acc, AT::lift_i(v, adelta));
+                }
+            } else {
+                agg_tagged(in, tin, imask, h, e, OpDyn{&P.st[n - 1]});
             }
         } else {
             const uint32_t tl = partial_stage<TAG, U8 && n == 1>(&P.st[n - 1], in, tin, imask, h, e, Q<n>(), T<n>(),
@@ -741,8 +814,9 @@ struct Pipe {
 
     // Region-id-keyed segmented reduction with a carry across ensembles
     // (tagged aggregate).  Ensembles may mix regions.
+    template <class Op>
     __device__ __forceinline__ void agg_tagged(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
-                                               uint32_t e) {
+                                               uint32_t e, const Op op) {
 #pragma unroll
         for (int j = 0; j < IPL; ++j) {
             const int cntj = (int)e - j * 32;
@@ -753,7 +827,10 @@ struct Pipe {
             if constexpr (U8) {
                 if (act && key != dkey) { dkey = key; adelta = part_delta(key); }
             }
-            const A val = act ? AT::lift_i(agg_load(in, h + idx, imask), adelta) : AT::id();
+            uint32_t x = act ? agg_load(in, h + idx, imask) : 0u;
+            const bool keep = act && op(x);          // fused node K: its op; else pass-all
+            if constexpr (NA) fkept += keep ? 1u : 0u;
+            const A val = keep ? AT::lift_i(x, adelta) : AT::id();
             if (__all_sync(kFull, !act || key == akey)) {
                 acc = AT::comb(acc, val);      // fast path: the whole slice continues the carry region
                 continue;
@@ -803,7 +880,7 @@ struct Pipe {
 
     template <int n>
     __device__ __forceinline__ bool fire_chain(bool drained) {
-        if constexpr (n > K + 1) {
+        if constexpr (n > (NA ? K : K + 1)) {
             return false;
         } else {
             const long long t0 = prof ? clock64() : 0;
@@ -817,7 +894,7 @@ struct Pipe {
     // Node n's items = positions it consumed on edge n-1; its data firings =
     // full ensembles + partial ensembles (counted separately in the header).
     template <int n = 1>
-    __device__ __forceinline__ void finish_counters() {
+    __device__ __forceinline__ void finish_counters(uint32_t fitems) {
         if constexpr (n <= K + 1) {
             if (lane == 0) {
                 // c[0] = partial ensembles, c[1] = their items (accumulated in the run)
@@ -828,16 +905,23 @@ struct Pipe {
                 c[1] = full;
                 c[2] = items;
                 c[3] = E<n - 1>().sh;                      // signals consumed
+                if constexpr (NA && n == K + 1) {          // fused aggregate: node K's firings,
+                    c[0] = c[-4];                          // the items that survived node K and
+                    c[1] = c[-3];                          // the signals node K consumed
+                    c[2] = fitems;
+                    c[3] = E<K - 1>().sh;
+                }
                 if constexpr (n == 1) {                     // enumerate: items / signals emitted
                     c[-4 + 2] = E<0>().qt - q_start[0];
                     c[-4 + 3] = E<0>().st;
                 }
             }
-            finish_counters<n + 1>();
+            finish_counters<n + 1>(fitems);
         }
     }
     __device__ __forceinline__ void flush_stats() {
-        finish_counters<1>();
+        const uint32_t fitems = NA ? __reduce_add_sync(kFull, fkept) : 0u;
+        finish_counters<1>(fitems);
         __syncwarp();
         if (lane < K + 2) {
             const uint32_t *c = reinterpret_cast<const uint32_t *>(base + 32) + 4 * lane;
@@ -897,12 +981,12 @@ struct Pipe {
     }
 };
 
-template <int K, int AGG, bool TAG>
+template <int K, int AGG, bool TAG, bool FUSE>
 __global__ void __launch_bounds__(WPB * 32, 1) k_pipeline(const __grid_constant__ KParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    using PP = Pipe<K, AGG, TAG>;
+    using PP = Pipe<K, AGG, TAG, FUSE>;
     uint8_t *mine = smem + (size_t)warp * PP::smem_bytes(P.qcap, P.scap, P.q0_stage);
     if (P.hdr->err) return;
     PP pipe(P, mine, lane);
