@@ -95,8 +95,7 @@ template <bool TAG, class Op, bool U8IN = false>
 __device__ __noinline__ uint32_t filter_batch(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                               uint32_t nens, uint32_t *out, uint32_t *tout, uint32_t qmask,
                                               uint32_t tl, const Op op, uint32_t lt, uint32_t cmask = 0) {
-    uint32_t k = 0;
-    for (; k < nens; ++k, h += W) filter_slices<TAG, IPL, Op, U8IN>(in, tin, imask, h, out, tout, qmask, tl, op, lt, cmask);
+    for (uint32_t k = 0; k < nens; ++k, h += W) filter_slices<TAG, IPL, Op, U8IN>(in, tin, imask, h, out, tout, qmask, tl, op, lt, cmask);
     __syncwarp();
     return tl;
 }
@@ -126,6 +125,35 @@ __device__ __noinline__ uint32_t partial_stage(const StageP *sp, const uint32_t 
     }
     __syncwarp();
     return tl;
+}
+
+// Fused terminal node, full ensembles, signal strategy (see Pipe::FUSE): the
+// node's op decides each item, survivors are folded into the per-lane
+// accumulator (isGood + a::run).  Out of line so the hot loop
+// stays one copy per op.
+template <class AT>
+struct FusedAcc {
+    typename AT::A acc;
+    uint32_t kept;
+};
+template <class AT, class Op, bool U8IN>
+__device__ __noinline__ FusedAcc<AT> fused_batch(const uint32_t *in, uint32_t imask, uint32_t h, uint32_t nens,
+                                                 const Op op, long long adelta, uint32_t cmask, FusedAcc<AT> st) {
+    const uint32_t lane = threadIdx.x & 31u;
+    for (uint32_t k = 0; k < nens; ++k, h += W) {
+        uint32_t v[IPL];
+#pragma unroll
+        for (int j = 0; j < IPL; ++j) v[j] = load_item<U8IN>(in, h + 32 * j + lane, imask, cmask);
+        typename AT::A part = AT::id();
+#pragma unroll
+        for (int j = 0; j < IPL; ++j) {
+            const bool keep = op(v[j]);
+            st.kept += keep ? 1u : 0u;
+            if (keep) part = AT::comb(part, AT::lift_i(v[j], adelta));
+        }
+        st.acc = AT::comb(st.acc, part);
+    }
+    return st;
 }
 
 struct Chunk {
@@ -624,19 +652,27 @@ struct Pipe {
     // survivors into the per-lane accumulator (isGood + a::run).
     template <class Op>
     __device__ __forceinline__ void fused_full(const uint32_t *in, uint32_t imask, uint32_t h, uint32_t nens, const Op op) {
-        for (uint32_t k = 0; k < nens; ++k, h += W) {
-            uint32_t v[IPL];
+        if constexpr (K == 1) {
+            // single-stage pipeline: inline (no other stage code competes for the
+            // instruction cache; fewer registers -> more instances per SM)
+            for (uint32_t k = 0; k < nens; ++k, h += W) {
+                uint32_t v[IPL];
 #pragma unroll
-            for (int j = 0; j < IPL; ++j) v[j] = agg_load(in, h + 32 * j + lane, imask);
-            A part = AT::id();
+                for (int j = 0; j < IPL; ++j) v[j] = agg_load(in, h + 32 * j + lane, imask);
+                A part = AT::id();
 #pragma unroll
-            for (int j = 0; j < IPL; ++j) {
-                const bool keep = op(v[j]);
-                fkept += keep ? 1u : 0u;
-                if (keep) part = AT::comb(part, AT::lift_i(v[j], adelta));
+                for (int j = 0; j < IPL; ++j) {
+                    const bool keep = op(v[j]);
+                    fkept += keep ? 1u : 0u;
+                    if (keep) part = AT::comb(part, AT::lift_i(v[j], adelta));
+                }
+                acc = AT::comb(acc, part);
             }
-            acc = AT::comb(acc, part);
+            return;
         }
+        const FusedAcc<AT> r = fused_batch<AT, Op, AGG_U8IN>(in, imask, h, nens, op, adelta, P.C - 1, FusedAcc<AT>{acc, fkept});
+        acc = r.acc;
+        fkept = r.kept;
     }
     template <class Op>
     __device__ __forceinline__ void fused_run(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
@@ -982,7 +1018,7 @@ struct Pipe {
 };
 
 template <int K, int AGG, bool TAG, bool FUSE>
-__global__ void __launch_bounds__(WPB * 32, 1) k_pipeline(const __grid_constant__ KParams P) {
+__global__ void __launch_bounds__(WPB * 32, 4) k_pipeline(const __grid_constant__ KParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
