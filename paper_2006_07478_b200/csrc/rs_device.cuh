@@ -107,6 +107,7 @@ struct AggT;
 
 template <>
 struct AggT<20> {  // RS_OP_SUM_I64 over int32 elements
+    static constexpr bool heavy = false;   // lift costs far more than a select (fused paths lift survivors only)
     using A = unsigned long long;  // two's-complement wraparound sum
     __device__ static A id() { return 0ull; }
     __device__ static A lift(uint32_t v) { return (A)(long long)(int)v; }
@@ -122,6 +123,7 @@ struct AggT<20> {  // RS_OP_SUM_I64 over int32 elements
 
 template <>
 struct AggT<21> {  // RS_OP_SUM_F32 over fp32 elements
+    static constexpr bool heavy = false;   // lift costs far more than a select (fused paths lift survivors only)
     using A = float;
     __device__ static A id() { return 0.0f; }
     __device__ static A lift(uint32_t v) { return __uint_as_float(v); }
@@ -137,6 +139,7 @@ struct AggT<21> {  // RS_OP_SUM_F32 over fp32 elements
 
 template <>
 struct AggT<22> {  // RS_OP_COUNT_MIN_U32 over uint32 elements: (count, min)
+    static constexpr bool heavy = false;   // lift costs far more than a select (fused paths lift survivors only)
     using A = uint2;
     __device__ static A id() { return make_uint2(0u, 0xffffffffu); }
     __device__ static A lift(uint32_t v) { return make_uint2(1u, v); }
@@ -170,6 +173,7 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
 
 template <>
 struct AggT<23> {  // RS_OP_COUNT_XOR64 over u8 elements: (count, xor of mix64(i << 8 | byte))
+    static constexpr bool heavy = true;   // lift costs far more than a select (fused paths lift survivors only)
     using A = ulonglong2;
     __device__ static A id() { return make_ulonglong2(0ull, 0ull); }
     // item = byte | (position mod C) << 8; delta = chunk base - region start, so the

@@ -131,6 +131,44 @@ __device__ __noinline__ uint32_t partial_stage(const StageP *sp, const uint32_t 
 // node's op decides each item, survivors are folded into the per-lane
 // accumulator (isGood + a::run).  Out of line so the hot loop
 // stays one copy per op.
+// Fold the survivors of one ensemble (v[j] kept iff bit j of km) into acc.
+// Cheap lifts: a select per slot.  Heavy lifts (the text hash): survivors are
+// sparse, so each lane lifts its first and second survivor under warp-uniform
+// guards and only a lane with three or more walks its slots again.
+template <class AT>
+__device__ __forceinline__ typename AT::A fold_kept(typename AT::A acc, const uint32_t (&v)[IPL], uint32_t km,
+                                                    long long adelta) {
+    if constexpr (!AT::heavy) {
+        typename AT::A part = AT::id();
+#pragma unroll
+        for (int j = 0; j < IPL; ++j)
+            if ((km >> j) & 1u) part = AT::comb(part, AT::lift_i(v[j], adelta));
+        return AT::comb(acc, part);
+    } else {
+        uint32_t s1 = 0, s2 = 0;
+        const uint32_t nk = __popc(km);
+#pragma unroll
+        for (int j = IPL - 1; j >= 0; --j) {       // s1 = first survivor, s2 = second
+            if ((km >> j) & 1u) { s2 = s1; s1 = v[j]; }
+        }
+        if (__any_sync(kFull, nk != 0))
+            if (nk != 0) acc = AT::comb(acc, AT::lift_i(s1, adelta));
+        if (__any_sync(kFull, nk > 1)) {
+            if (nk > 1) acc = AT::comb(acc, AT::lift_i(s2, adelta));
+            if (__any_sync(kFull, nk > 2)) {
+                uint32_t seen = 0;
+#pragma unroll
+                for (int j = 0; j < IPL; ++j)
+                    if ((km >> j) & 1u) {
+                        if (seen >= 2) acc = AT::comb(acc, AT::lift_i(v[j], adelta));
+                        ++seen;
+                    }
+            }
+        }
+        return acc;
+    }
+}
+
 template <class AT>
 struct FusedAcc {
     typename AT::A acc;
@@ -144,14 +182,11 @@ __device__ __noinline__ FusedAcc<AT> fused_batch(const uint32_t *in, uint32_t im
         uint32_t v[IPL];
 #pragma unroll
         for (int j = 0; j < IPL; ++j) v[j] = load_item<U8IN>(in, h + 32 * j + lane, imask, cmask);
-        typename AT::A part = AT::id();
+        uint32_t km = 0;
 #pragma unroll
-        for (int j = 0; j < IPL; ++j) {
-            const bool keep = op(v[j]);
-            st.kept += keep ? 1u : 0u;
-            if (keep) part = AT::comb(part, AT::lift_i(v[j], adelta));
-        }
-        st.acc = AT::comb(st.acc, part);
+        for (int j = 0; j < IPL; ++j) km |= op(v[j]) ? 1u << j : 0u;
+        st.kept += __popc(km);
+        st.acc = fold_kept<AT>(st.acc, v, km, adelta);
     }
     return st;
 }
@@ -659,14 +694,22 @@ struct Pipe {
                 uint32_t v[IPL];
 #pragma unroll
                 for (int j = 0; j < IPL; ++j) v[j] = agg_load(in, h + 32 * j + lane, imask);
-                A part = AT::id();
+                if constexpr (AT::heavy) {
+                    uint32_t km = 0;
 #pragma unroll
-                for (int j = 0; j < IPL; ++j) {
-                    const bool keep = op(v[j]);
-                    fkept += keep ? 1u : 0u;
-                    if (keep) part = AT::comb(part, AT::lift_i(v[j], adelta));
+                    for (int j = 0; j < IPL; ++j) km |= op(v[j]) ? 1u << j : 0u;
+                    fkept += __popc(km);
+                    acc = fold_kept<AT>(acc, v, km, adelta);
+                } else {
+                    A part = AT::id();
+#pragma unroll
+                    for (int j = 0; j < IPL; ++j) {
+                        const bool keep = op(v[j]);
+                        fkept += keep ? 1u : 0u;
+                        if (keep) part = AT::comb(part, AT::lift_i(v[j], adelta));
+                    }
+                    acc = AT::comb(acc, part);
                 }
-                acc = AT::comb(acc, part);
             }
             return;
         }
@@ -829,14 +872,15 @@ struct Pipe {
         } else if constexpr (NA && n == K) {
             if constexpr (!TAG) {
                 const OpDyn op{&P.st[n - 1]};
+                uint32_t v[IPL], km = 0;
 #pragma unroll
                 for (int j = 0; j < IPL; ++j) {
                     const uint32_t idx = j * 32 + lane;
-                    uint32_t v = idx < e ? agg_load(in, h + idx, imask) : 0u;
-                    const bool keep = idx < e && op(v);
-                    fkept += keep ? 1u : 0u;
-                    if (keep) acc = AT::comb(acc, AT::lift_i(v, adelta));
+                    v[j] = idx < e ? agg_load(in, h + idx, imask) : 0u;
+                    km |= (idx < e && op(v[j])) ? 1u << j : 0u;
                 }
+                fkept += __popc(km);
+                acc = fold_kept<AT>(acc, v, km, adelta);
             } else {
                 agg_tagged(in, tin, imask, h, e, OpDyn{&P.st[n - 1]});
             }

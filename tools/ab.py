@@ -20,6 +20,17 @@ for L in (4096, 256):
         for i in range(6):
             p.run(vals, off, out, ws); ms.append(p.kernel_times()[1])
         res[f"L{L}K{K}"] = statistics.median(ms[1:])
+if os.environ.get("AB_TEXT"):
+    del vals
+    b, toff = synth.torch_text(1 << 30, seed=4)
+    R = toff.numel() - 1
+    for strat in ("signal", "tagged"):
+        p = rs.Pipeline(synth.text_stages(), "count_xor64", strategy=strat, flags=rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING)
+        out = p.alloc_outputs(R); ws = p.alloc_workspace(R, b.numel())
+        ms = []
+        for i in range(6):
+            p.run(b, toff, out, ws); ms.append(p.kernel_times()[1])
+        res[f"text_{strat}"] = statistics.median(ms[1:])
 print(json.dumps(res))
 '''
 out = {l: [] for l in libs}
