@@ -872,15 +872,26 @@ struct Pipe {
         } else if constexpr (NA && n == K) {
             if constexpr (!TAG) {
                 const OpDyn op{&P.st[n - 1]};
-                uint32_t v[IPL], km = 0;
+                if constexpr (AT::heavy) {
+                    uint32_t v[IPL], km = 0;
 #pragma unroll
-                for (int j = 0; j < IPL; ++j) {
-                    const uint32_t idx = j * 32 + lane;
-                    v[j] = idx < e ? agg_load(in, h + idx, imask) : 0u;
-                    km |= (idx < e && op(v[j])) ? 1u << j : 0u;
+                    for (int j = 0; j < IPL; ++j) {
+                        const uint32_t idx = j * 32 + lane;
+                        v[j] = idx < e ? agg_load(in, h + idx, imask) : 0u;
+                        km |= (idx < e && op(v[j])) ? 1u << j : 0u;
+                    }
+                    fkept += __popc(km);
+                    acc = fold_kept<AT>(acc, v, km, adelta);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < IPL; ++j) {
+                        const uint32_t idx = j * 32 + lane;
+                        uint32_t v = idx < e ? agg_load(in, h + idx, imask) : 0u;
+                        const bool keep = idx < e && op(v);
+                        fkept += keep ? 1u : 0u;
+                        if (keep) acc = AT::comb(acc, AT::lift_i(v, adelta));
+                    }
                 }
-                fkept += __popc(km);
-                acc = fold_kept<AT>(acc, v, km, adelta);
             } else {
                 agg_tagged(in, tin, imask, h, e, OpDyn{&P.st[n - 1]});
             }

@@ -10,7 +10,7 @@ import paper_2006_07478_b200 as rs
 N = 1 << 29
 vals = synth.torch_values(N, "i32", seed=1)
 res = {}
-for L in (4096, 256):
+for L in ((4096, 256) if not os.environ.get("AB_NOSWEEP") else ()):
     lens = torch.full((N // L,), L, dtype=torch.int64, device="cuda")
     off = synth.torch_offsets(lens); R = off.numel() - 1
     for K in (3, 1):
@@ -21,7 +21,6 @@ for L in (4096, 256):
             p.run(vals, off, out, ws); ms.append(p.kernel_times()[1])
         res[f"L{L}K{K}"] = statistics.median(ms[1:])
 if os.environ.get("AB_TEXT"):
-    del vals
     b, toff = synth.torch_text(1 << 30, seed=4)
     R = toff.numel() - 1
     for strat in ("signal", "tagged"):
@@ -31,6 +30,16 @@ if os.environ.get("AB_TEXT"):
         for i in range(6):
             p.run(b, toff, out, ws); ms.append(p.kernel_times()[1])
         res[f"text_{strat}"] = statistics.median(ms[1:])
+if os.environ.get("AB_GRAPH"):
+    w, goff = synth.torch_rmat_csr(24, 16, seed=3)
+    R = goff.numel() - 1
+    for strat in ("signal", "tagged"):
+        p = rs.Pipeline([("lt_u32", 1 << 31)], "count_min_u32", strategy=strat, flags=rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING)
+        out = p.alloc_outputs(R); ws = p.alloc_workspace(R, w.numel())
+        ms = []
+        for i in range(6):
+            p.run(w, goff, out, ws); ms.append(p.kernel_times()[1])
+        res[f"graph_{strat}"] = statistics.median(ms[1:])
 print(json.dumps(res))
 '''
 out = {l: [] for l in libs}
