@@ -31,7 +31,9 @@ def rs():
 
 
 def run_gpu(rs, vals, off, stages, agg, strategy="signal", mode="seq", **cfg):
-    flags = rs.RS_FLAG_STATS | (rs.RS_FLAG_WARP_SPECIALIZED if mode == "ws" else 0)
+    # modes: "seq" (default: sequential scheduler, aggregate fused into the last
+    # stage), "unfused" (sequential, separate AGGREGATE node), "ws" (warp-specialised)
+    flags = rs.RS_FLAG_STATS | {"ws": rs.RS_FLAG_WARP_SPECIALIZED, "unfused": rs.RS_FLAG_UNFUSED}.get(mode, 0)
     p = rs.Pipeline(stages, agg, strategy=strategy, flags=flags, **cfg)
     dev = torch.device("cuda:0")
     e = torch.from_numpy(np.ascontiguousarray(vals)).to(dev)
@@ -113,7 +115,7 @@ def _case(seed, agg, R=None, dist=None, L=None, base=None):
 
 @pytest.mark.parametrize("seed", range(24))
 @pytest.mark.parametrize("strategy", ["signal", "tagged"])
-@pytest.mark.parametrize("mode", ["ws", "seq"])
+@pytest.mark.parametrize("mode", ["ws", "seq", "unfused"])
 def test_random_parity(rs, seed, strategy, mode):
     agg = ["sum_i64", "sum_f32", "count_min_u32"][seed % 3]
     vals, off, stages = _case(seed, agg)
@@ -128,7 +130,7 @@ def test_random_parity(rs, seed, strategy, mode):
 
 @pytest.mark.parametrize("strategy", ["signal", "tagged"])
 @pytest.mark.parametrize("L", [1, 4, 32, 127, 128, 129, 256, 4096, 100000])
-@pytest.mark.parametrize("mode", ["ws", "seq"])
+@pytest.mark.parametrize("mode", ["ws", "seq", "unfused"])
 def test_region_lengths(rs, strategy, L, mode):
     """Region lengths 1..4096 (north star) plus regions far longer than a chunk."""
     N = 1 << 18
@@ -199,13 +201,13 @@ def test_grid_and_capacity_invariance(rs):
     for cfg in (dict(grid=1), dict(grid=2, chunk=2048), dict(queue_cap=1024, signal_cap=8), dict(signal_cap=4),
                 dict(queue_cap=256)):
         for strat in ("signal", "tagged"):
-            for mode in ("ws", "seq"):
+            for mode in ("ws", "seq", "unfused"):
                 got, _, _ = run_gpu(rs, vals, off, stages, "sum_i64", strat, mode, **cfg)
                 assert_parity(got, ref, "sum_i64")
 
 
 @pytest.mark.parametrize("R", [32, 64, 96, 128, 256, 512, 1024])
-@pytest.mark.parametrize("mode", ["ws", "seq"])
+@pytest.mark.parametrize("mode", ["ws", "seq", "unfused"])
 def test_occupancy_closed_form_gpu(rs, R, mode):
     """One instance (grid=1), fixed regions dividing the chunk, pass-all
     stages, full-first: the aggregate's lane fraction equals R/(w ceil(R/w))
@@ -302,10 +304,12 @@ def test_full_size_sampled(rs, strategy):
         torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("mode", ["seq", "unfused"])
 @pytest.mark.parametrize("strategy", ["signal", "tagged"])
 @pytest.mark.parametrize("line_mean,cls,base,chunk", [
-    (1397.0, b"{", 0, 8192), (1397.0, b"{", 7, 2048), (20.0, b"{0123456789", 13, 2048), (5000.0, b"", 3, 2048)])
-def test_text_count_xor64(rs, strategy, line_mean, cls, base, chunk):
+    (1397.0, b"{", 0, 8192), (1397.0, b"{", 7, 2048), (20.0, b"{0123456789", 13, 2048), (5000.0, b"", 3, 2048),
+    (64.0, bytes(range(48, 58)) + b"{", 1, 2048)])
+def test_text_count_xor64(rs, strategy, line_mean, cls, base, chunk, mode):
     """D4 shape: byte stream split on newlines, CLASS filter, COUNT + XOR64 of
     mix64(i << 8 | byte) per line (reading A19) -- bit-exact; lines longer than
     a chunk, unaligned starts (16-byte TMA blocks), and no filter at all (the
@@ -316,14 +320,15 @@ def test_text_count_xor64(rs, strategy, line_mean, cls, base, chunk):
         off = off + base
     stages = [("class", synth.class_table(cls))] if cls else []
     ref = oracle.brute(b, off, stages, "count_xor64")
-    got, st, _ = run_gpu(rs, b, off, stages, "count_xor64", strategy, chunk=chunk)
+    got, st, _ = run_gpu(rs, b, off, stages, "count_xor64", strategy, mode, chunk=chunk)
     got = [g.view(np.uint64) for g in got]
     assert_parity(got, ref, "count_xor64")
     assert st[0][2] == off[-1] - off[0]
 
 
+@pytest.mark.parametrize("mode", ["seq", "unfused"])
 @pytest.mark.parametrize("strategy", ["signal", "tagged"])
-def test_graph_rmat_count_min(rs, strategy):
+def test_graph_rmat_count_min(rs, strategy, mode):
     """D3 shape: edges grouped by source vertex of an R-MAT graph (skewed
     degrees: most vertices empty, a few with thousands of edges spanning
     chunks), LT(2^31) weight filter, COUNT + MIN per vertex -- bit-exact."""
@@ -332,6 +337,6 @@ def test_graph_rmat_count_min(rs, strategy):
     offh = off.cpu().numpy()
     stages = [("lt_u32", 1 << 31)]
     ref = oracle.brute(wv, offh, stages, "count_min_u32")
-    got, st, _ = run_gpu(rs, wv, offh, stages, "count_min_u32", strategy, chunk=2048)
+    got, st, _ = run_gpu(rs, wv, offh, stages, "count_min_u32", strategy, mode, chunk=2048)
     assert_parity(got, ref, "count_min_u32")
     assert (np.diff(offh) == 0).mean() > 0.3          # R-MAT: many isolated vertices
