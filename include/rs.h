@@ -114,13 +114,20 @@ enum {
 typedef struct {
     int32_t strategy;        /* rs_strategy                                          */
     uint32_t simd_width;     /* ensemble capacity w in items; only 128 is built */
-    uint32_t queue_cap;      /* inter-stage data queue capacity (items, power of 2, >= 2w; 0 = auto: 8w with 2+ stages, else 16w) */
+    uint32_t queue_cap;      /* data queue capacity (items, power of 2 in [2w, 65536]).  4-byte elements,
+                                sequential scheduler: all queues share ONE in-place ring of
+                                max(4*q0_stage, min(queue_cap, 8*q0_stage)) items, raised to fit one
+                                partial ensemble per queue plus a stage (0 = auto: 32w signal, 16w
+                                tagged).  u8 elements or RS_FLAG_WARP_SPECIALIZED: capacity of each
+                                inter-stage queue (0 = auto: 8w with 2+ stages, else 16w). */
     uint32_t signal_cap;     /* signal queue capacity (entries, power of 2, >= 4; 0 = auto) */
     int32_t grid;            /* persistent CTAs; 0 = fill the device                  */
     uint32_t chunk;          /* children per parent-stream claim; 0 = default        */
     uint32_t flags;          /* RS_FLAG_*                                            */
-    uint32_t q0_stage;       /* elements per TMA stage of the enumerate queue (4 stages);
-                                power of 2 in [128, 4096]; 0 = auto (256 tagged or 2+ stages, else 512) */
+    uint32_t q0_stage;       /* elements per TMA stage of the enumerate queue (the ring holds 4..8
+                                stages); power of 2 in [128, 4096], <= chunk; 0 = auto (in-place
+                                rings: 1024 signal, 512 tagged; otherwise 256 tagged or 2+ stages,
+                                else 512) */
 } rs_config;
 
 /* Per-node occupancy counters (§2.2, §5).  Node 0 is the

@@ -149,9 +149,16 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     // scheduler for short pipelines; with 2+ stages a smaller footprint fits
     // twice the instances per SM, which wins.
     const int nst_ = n_nodes - 2;
-    if (cfg.queue_cap == 0) cfg.queue_cap = nst_ >= 2 ? 8 * W : 16 * W;
+    // In-place pipelines (4-byte elements, sequential scheduler): all queues
+    // share one ring of queue_cap items fed by TMA stages of q0_stage; a big
+    // ring amortises the scheduler, the tag ring doubles the tagged footprint
+    // (profiles/r1_tuning.txt, tools/tune4.py).
+    const bool inplace = elem != RS_U8 && !(cfg.flags & RS_FLAG_WARP_SPECIALIZED);
+    const bool tagged_ = cfg.strategy == RS_STRATEGY_TAGGED;
+    if (cfg.queue_cap == 0) cfg.queue_cap = inplace ? (tagged_ ? 16 * W : 32 * W) : (nst_ >= 2 ? 8 * W : 16 * W);
     if (cfg.signal_cap == 0) cfg.signal_cap = nst_ >= 2 ? 64 : 128;
-    if (cfg.q0_stage == 0) cfg.q0_stage = (cfg.strategy == RS_STRATEGY_TAGGED || nst_ >= 2) ? 256 : 512;
+    if (cfg.q0_stage == 0)
+        cfg.q0_stage = inplace ? (tagged_ ? 512 : 1024) : ((tagged_ || nst_ >= 2) ? 256 : 512);
     if (!is_pow2(cfg.queue_cap) || cfg.queue_cap < 2 * W || cfg.queue_cap > 65536)
         return fail(RS_ERR_UNSUPPORTED, "queue_cap must be a power of 2 in [256, 65536]");
     if (!is_pow2(cfg.signal_cap) || cfg.signal_cap < 4 || cfg.signal_cap > 65536)
@@ -162,7 +169,7 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     if (cfg.grid < 0) return fail(RS_ERR_INVALID_ARG, "grid must be >= 0");
     if (!is_pow2(cfg.q0_stage) || cfg.q0_stage < 128 || cfg.q0_stage > 4096)
         return fail(RS_ERR_UNSUPPORTED, "q0_stage must be a power of 2 in [128, 4096]");
-    if (cfg.chunk < NST * cfg.q0_stage) return fail(RS_ERR_UNSUPPORTED, "chunk must be >= 4 * q0_stage");
+    if (cfg.chunk < cfg.q0_stage) return fail(RS_ERR_UNSUPPORTED, "chunk must be >= q0_stage");   // stages never straddle chunks
     rs_pipeline *p = new rs_pipeline();
     p->cfg = cfg;
     p->elem = elem;
@@ -291,6 +298,7 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
     K.qcap = p->cfg.queue_cap;
     K.scap = p->cfg.signal_cap;
     K.q0_stage = p->cfg.q0_stage;
+    K.ring0 = L.ring0;
     K.esize = p->elem == RS_U8 ? 1u : 4u;
     K.flags = p->cfg.flags;
     K.tagged = p->cfg.strategy == RS_STRATEGY_TAGGED;

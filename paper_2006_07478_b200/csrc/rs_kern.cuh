@@ -39,7 +39,8 @@ constexpr int IPL = W / 32;         // items per lane per ensemble
 constexpr uint32_t SLOT = 0x80000000u;  // key bit: partial-aggregate slot instead of region id
 constexpr uint32_t END_BIT = 0x80000000u;  // signal word: kind End
 constexpr int MAXK = 4;             // max FILTER/TRANSFORM stages
-constexpr int NST = 4;              // TMA stages in the Q0 ring
+constexpr int NST = 4;              // TMA stages in the Q0 ring (warp-specialised kernel; separate-queue rings)
+constexpr int NSTMAX = 8;           // TMA stages of an in-place ring (sequential kernel)
 constexpr int WPB = 4;              // warps (instances) per CTA
 
 enum : int32_t { ERR_OFFSETS = 1, ERR_WATCHDOG = 2, ERR_SIGFULL = 3, ERR_UNMATCHED = 4, ERR_QFULL = 5, ERR_LIMIT = 7 };
@@ -74,6 +75,7 @@ struct KParams {
     uint32_t C;                     // chunk length (children)
     uint32_t qcap, scap;            // queue / signal capacities (powers of 2)
     uint32_t q0_stage;              // Q0 TMA stage size in elements (sequential kernel)
+    uint32_t ring0;                 // Q0 ring capacity in elements (sequential kernel; in-place: all queues)
     uint32_t esize;                 // element size in bytes (1 = u8 text, else 4)
     uint32_t flags;
     int32_t tagged;
@@ -190,6 +192,7 @@ struct Launch {
     void (*pre)(KParams, int);
     void (*fix)(KParams);
     uint32_t inst_bytes;
+    uint32_t ring0;                 // Q0 ring capacity (elements) of the sequential kernel
     int out_bytes0, out_bytes1;
 };
 
@@ -234,13 +237,24 @@ uint32_t smem_ws(int K, uint32_t qcap, uint32_t scap) {
 }
 
 template <int AGG, bool TAG, bool FUSE>
-uint32_t smem_for(int K, uint32_t qcap, uint32_t scap, uint32_t sblk) {
+uint32_t ring_for(int K, uint32_t sblk, uint32_t qcap) {
     switch (K) {
-        case 0: return Pipe<0, AGG, TAG, false>::smem_bytes(qcap, scap, sblk);
-        case 1: return Pipe<1, AGG, TAG, FUSE>::smem_bytes(qcap, scap, sblk);
-        case 2: return Pipe<2, AGG, TAG, FUSE>::smem_bytes(qcap, scap, sblk);
-        case 3: return Pipe<3, AGG, TAG, FUSE>::smem_bytes(qcap, scap, sblk);
-        default: return Pipe<4, AGG, TAG, FUSE>::smem_bytes(qcap, scap, sblk);
+        case 0: return Pipe<0, AGG, TAG, false>::ring_for(sblk, qcap);
+        case 1: return Pipe<1, AGG, TAG, FUSE>::ring_for(sblk, qcap);
+        case 2: return Pipe<2, AGG, TAG, FUSE>::ring_for(sblk, qcap);
+        case 3: return Pipe<3, AGG, TAG, FUSE>::ring_for(sblk, qcap);
+        default: return Pipe<4, AGG, TAG, FUSE>::ring_for(sblk, qcap);
+    }
+}
+
+template <int AGG, bool TAG, bool FUSE>
+uint32_t smem_for(int K, uint32_t qcap, uint32_t scap, uint32_t ring) {
+    switch (K) {
+        case 0: return Pipe<0, AGG, TAG, false>::smem_bytes(qcap, scap, ring);
+        case 1: return Pipe<1, AGG, TAG, FUSE>::smem_bytes(qcap, scap, ring);
+        case 2: return Pipe<2, AGG, TAG, FUSE>::smem_bytes(qcap, scap, ring);
+        case 3: return Pipe<3, AGG, TAG, FUSE>::smem_bytes(qcap, scap, ring);
+        default: return Pipe<4, AGG, TAG, FUSE>::smem_bytes(qcap, scap, ring);
     }
 }
 
@@ -254,8 +268,11 @@ Launch launch_for(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint
     L.ws_bytes = tag ? smem_ws<AGG, true>(K, qcap, scap) : smem_ws<AGG, false>(K, qcap, scap);
     L.pre = k_prepass<AGG>;
     L.fix = k_fixup<AGG>;
-    L.inst_bytes = tag ? (fuse ? smem_for<AGG, true, true>(K, qcap, scap, sblk) : smem_for<AGG, true, false>(K, qcap, scap, sblk))
-                       : (fuse ? smem_for<AGG, false, true>(K, qcap, scap, sblk) : smem_for<AGG, false, false>(K, qcap, scap, sblk));
+    L.ring0 = tag ? (fuse ? ring_for<AGG, true, true>(K, sblk, qcap) : ring_for<AGG, true, false>(K, sblk, qcap))
+                  : (fuse ? ring_for<AGG, false, true>(K, sblk, qcap) : ring_for<AGG, false, false>(K, sblk, qcap));
+    const uint32_t r = L.ring0;
+    L.inst_bytes = tag ? (fuse ? smem_for<AGG, true, true>(K, qcap, scap, r) : smem_for<AGG, true, false>(K, qcap, scap, r))
+                       : (fuse ? smem_for<AGG, false, true>(K, qcap, scap, r) : smem_for<AGG, false, false>(K, qcap, scap, r));
     L.out_bytes0 = AggT<AGG>::bytes0;
     L.out_bytes1 = AggT<AGG>::bytes1;
     return L;

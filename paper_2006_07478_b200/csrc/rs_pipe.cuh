@@ -74,6 +74,7 @@ __device__ __forceinline__ void filter_slices(const uint32_t *in, const uint32_t
     if constexpr (TAG) {
 #pragma unroll
         for (int j = 0; j < NS; ++j) tg[j] = tin[(h + 32 * j + lane) & imask];
+        __syncwarp();   // in-place rings: tag reads of all lanes precede the tag stores below
     }
 #pragma unroll
     for (int j = 0; j < NS; ++j) keep[j] = op(v[j]);
@@ -113,7 +114,10 @@ __device__ __noinline__ uint32_t partial_stage(const StageP *sp, const uint32_t 
         const bool act = idx < e;
         uint32_t v = act ? load_item<U8IN>(in, h + idx, imask, cmask) : 0u;
         uint32_t tg = 0;
-        if constexpr (TAG) tg = act ? tin[(h + idx) & imask] : 0u;
+        if constexpr (TAG) {
+            tg = act ? tin[(h + idx) & imask] : 0u;
+            __syncwarp();   // in-place rings: tag reads precede the tag stores
+        }
         const bool keep = act && stage_apply(*sp, v);
         const uint32_t mk = __ballot_sync(kFull, keep);   // stable compaction
         if (keep) {
@@ -191,6 +195,38 @@ __device__ __noinline__ FusedAcc<AT> fused_batch(const uint32_t *in, uint32_t im
     return st;
 }
 
+// In-place rings: move n items (and tags) ending at position `end` up by
+// `shift` positions -- a memmove toward higher positions in blocks of <= w
+// items, highest block first (each block is read completely before it is
+// written, so overlapping source and destination are safe).
+template <bool TAG>
+__device__ __noinline__ void move_items(uint32_t *q, uint32_t *tq, uint32_t end, uint32_t n, uint32_t shift, uint32_t m) {
+    const uint32_t lane = threadIdx.x & 31u;
+    while (n > 0) {
+        const uint32_t c = n < (uint32_t)W ? n : (uint32_t)W;
+        const uint32_t s0 = end - c;
+        uint32_t v[IPL], tg[IPL];
+#pragma unroll
+        for (int j = 0; j < IPL; ++j) {
+            const uint32_t idx = 32 * j + lane;
+            v[j] = idx < c ? q[(s0 + idx) & m] : 0u;
+            if constexpr (TAG) tg[j] = idx < c ? tq[(s0 + idx) & m] : 0u;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < IPL; ++j) {
+            const uint32_t idx = 32 * j + lane;
+            if (idx < c) {
+                q[(s0 + shift + idx) & m] = v[j];
+                if constexpr (TAG) tq[(s0 + shift + idx) & m] = tg[j];
+            }
+        }
+        __syncwarp();
+        end -= c;
+        n -= c;
+    }
+}
+
 struct Chunk {
     int32_t k;             // chunk id (-1 = empty slot)
     long long beg, end;    // element range [beg, end)
@@ -218,20 +254,31 @@ struct Pipe {
     static constexpr uint32_t default_stage() { return TAG ? 256u : 512u; }
     static constexpr bool U8 = (AGG == 23);          // text stream: byte elements
     static constexpr uint32_t ESZ = U8 ? 1u : 4u;    // element size in the Q0 ring (bytes)
-    __host__ __device__ static constexpr uint32_t q0_bytes(uint32_t sblk) { return (NST * sblk * ESZ + 15u) & ~15u; }
-    // per-instance shared header: [0,32) TMA barriers, [32,128) node counters
+    // INPLACE (4-byte elements): every data queue Q_0..Q_NQ lives in ONE ring.
+    // Positions of all edges share the ring's coordinates and each FILTER/
+    // TRANSFORM node writes its survivors behind its own read head (stable
+    // compaction never outruns the reads: t_{e+1} <= h_e), so queue space is
+    // implied and a sweep can move a whole ring of items.
+    // Leftover partial ensembles are moved up behind the next head when the
+    // dead space between queues grows (relocate()).  Byte streams (text) keep
+    // one ring per queue: 1-byte inputs become 4-byte items.
+    static constexpr bool INPLACE = !U8;
+    __host__ __device__ static constexpr uint32_t q0_bytes(uint32_t ring) { return (ring * ESZ + 15u) & ~15u; }
+    // per-instance shared header: [0,64) TMA barriers, [64,160) node counters
     // (u32 x 24: data firings, full firings, items, signals per node),
-    // [128,256) RS_FLAG_PROFILE cycle counters (u64 x 16)
-    static constexpr uint32_t HDR = 256;
+    // [160,288) RS_FLAG_PROFILE cycle counters (u64 x 16)
+    static constexpr uint32_t HDR = 288;
+    static constexpr uint32_t CNT_OFF = 64, PROF_OFF = 160;
 
     const KParams &P;
     const int lane;
     const uint32_t lt;             // %lanemask_lt
     // shared-memory rings
     uint8_t *base;                 // this instance's shared-memory window
-    uint64_t *bar;                 // [NST] TMA stage barriers
+    uint64_t *bar;                 // [nstg] TMA stage barriers
     uint32_t qmask, smask, qcap, scap;
-    uint32_t sblk, ring0;          // Q0: TMA stage size (elements) and ring capacity (NST stages)
+    uint32_t sblk, ring0;          // Q0: TMA stage size (elements) and ring capacity (nstg stages)
+    uint32_t nstg, nsh;            // TMA stages in the ring (power of 2) and log2
 
     // Edge e (node e -> node e+1).  Kept as named scalars (not arrays) so the
     // whole state lives in registers.
@@ -254,27 +301,31 @@ struct Pipe {
     }
     // node counters live in the shared header (lane 0 updates them)
     __device__ __forceinline__ void stat_add(int n, int f, uint32_t v) const {
-        if (lane == 0) reinterpret_cast<uint32_t *>(base + 32)[4 * n + f] += v;
+        if (lane == 0) reinterpret_cast<uint32_t *>(base + CNT_OFF)[4 * n + f] += v;
     }
     __device__ __forceinline__ void pcnt(int i, unsigned long long v) const {
-        if (lane == 0) reinterpret_cast<unsigned long long *>(base + 128)[i] += v;
+        if (lane == 0) reinterpret_cast<unsigned long long *>(base + PROF_OFF)[i] += v;
     }
-    // ring addresses: Q0 (ring0 items) then Q_1..Q_K (qcap items), each followed
-    // by its tag ring in the tagged strategy, then the signal rings.
+    // ring addresses: Q0 (ring0 items) then -- separate-queue layout only --
+    // Q_1..Q_NQ (qcap items), each followed by its tag ring in the tagged
+    // strategy, then the signal rings.  In-place: every Q_e is the Q0 ring.
+    static constexpr uint32_t NQS = INPLACE ? 0 : NQ;   // separate shared-memory queues
     template <int e> __device__ __forceinline__ uint32_t *Q() const {
-        if constexpr (e == 0) return reinterpret_cast<uint32_t *>(base + HDR);
-        else return reinterpret_cast<uint32_t *>(base + HDR + q0_bytes(sblk) + (TAG ? ring0 * 4 : 0) +
+        if constexpr (e == 0 || INPLACE) return reinterpret_cast<uint32_t *>(base + HDR);
+        else return reinterpret_cast<uint32_t *>(base + HDR + q0_bytes(ring0) + (TAG ? ring0 * 4 : 0) +
                                                  (e - 1) * qcap * 4 * (TAG ? 2 : 1));
     }
     template <int e> __device__ __forceinline__ uint32_t *T() const {
         if constexpr (!TAG) return nullptr;
-        else if constexpr (e == 0) return reinterpret_cast<uint32_t *>(base + HDR + q0_bytes(sblk));
+        else if constexpr (e == 0 || INPLACE) return reinterpret_cast<uint32_t *>(base + HDR + q0_bytes(ring0));
         else return Q<e>() + qcap;
     }
     template <int e> __device__ __forceinline__ uint2 *S() const {
-        return reinterpret_cast<uint2 *>(base + HDR + q0_bytes(sblk) + (TAG ? ring0 * 4 : 0) + NQ * qcap * 4 * (TAG ? 2 : 1)) +
+        return reinterpret_cast<uint2 *>(base + HDR + q0_bytes(ring0) + (TAG ? ring0 * 4 : 0) + NQS * qcap * 4 * (TAG ? 2 : 1)) +
                e * scap;
     }
+    // ring index mask of edge e's queue
+    template <int e> __device__ __forceinline__ uint32_t qm() const { return (e == 0 || INPLACE) ? ring0 - 1 : qmask; }
 
     Chunk F0, F1;                      // chunk being enumerated, chunk staged next
     bool claims_done, enum_done;
@@ -307,14 +358,15 @@ struct Pipe {
         qmask = qcap - 1;
         smask = scap - 1;
         sblk = P.q0_stage;
-        ring0 = NST * sblk;
+        ring0 = P.ring0;
+        nstg = ring0 / sblk;
+        nsh = 31 - __clz(nstg);
         base = smem;
         bar = reinterpret_cast<uint64_t *>(smem);
         E0 = E1 = E2 = E3 = E4 = EdgeS{0u, 0u, 0u, 0u, 0u, 0u, false};
 #pragma unroll
         for (int e = 0; e <= K; ++e) q_start[e] = 0u;
-        if (lane == 0)
-            for (int i = 8; i < 64; ++i) reinterpret_cast<uint32_t *>(base)[i] = 0u;   // counters + profile
+        for (int i = 16 + lane; i < (int)(HDR / 4); i += 32) reinterpret_cast<uint32_t *>(base)[i] = 0u;   // counters + profile
         __syncwarp();
         F0.k = F1.k = -1;
         claims_done = enum_done = false;
@@ -335,9 +387,22 @@ struct Pipe {
         nchunks = P.hdr->nchunks;
     }
 
-    __host__ __device__ static constexpr uint32_t smem_bytes(uint32_t qcap, uint32_t scap, uint32_t sblk) {
-        return HDR + q0_bytes(sblk) + (TAG ? NST * sblk * 4 : 0) + NQ * qcap * 4 * (TAG ? 2 : 1) +
+    __host__ __device__ static constexpr uint32_t smem_bytes(uint32_t qcap, uint32_t scap, uint32_t ring) {
+        return HDR + q0_bytes(ring) + (TAG ? ring * 4 : 0) + NQS * qcap * 4 * (TAG ? 2 : 1) +
                (TAG ? 0 : NSG * scap * 8);
+    }
+    // Ring capacity: 4 TMA stages; in-place, the configured queue capacity
+    // (the one ring all queues share), at most NSTMAX stages, and at least one
+    // partial ensemble per queue plus a stage, so the TMA can always make
+    // progress (leftovers of < w items per queue are all that can stay behind;
+    // see relocate()).
+    __host__ static uint32_t ring_for(uint32_t sblk, uint32_t qcap) {
+        uint32_t r = 4 * sblk;
+        if (INPLACE) {
+            while (r < qcap && r < NSTMAX * sblk) r <<= 1;
+            while (r < (NQ + 1) * (uint32_t)W + sblk) r <<= 1;
+        }
+        return r;
     }
 
     // ---------------------------------------------------------- chunks
@@ -369,7 +434,7 @@ struct Pipe {
         const uint32_t n = min(sblk, c.pos + flen(c) - p0);
         const long long src = c.beg + (long long)p0 - (long long)c.pos;   // 16-byte aligned element index
         uint8_t *dst = reinterpret_cast<uint8_t *>(Q<0>()) + (size_t)(p0 & (ring0 - 1)) * ESZ;
-        uint64_t *b = &bar[j % NST];
+        uint64_t *b = &bar[j & (nstg - 1)];
         const long long lim = (P.n_elems - src) & ~(long long)(AL - 1);   // whole 16-byte blocks in the array
         const uint32_t ntma = (uint32_t)min((long long)((n + AL - 1) & ~(AL - 1)), lim);
         // tail elements that a 16-byte copy cannot reach without overrunning n_elems
@@ -379,6 +444,10 @@ struct Pipe {
             else reinterpret_cast<uint32_t *>(dst)[ntma + lane] =
                 __ldg(reinterpret_cast<const uint32_t *>(P.elems) + src + ntma + lane);
         }
+        // in-place rings: the slots being refilled may hold items every lane
+        // wrote through the generic proxy (compaction, relocation); order those
+        // writes before the async-proxy (TMA) writes of this stage
+        if constexpr (INPLACE) fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
             fence_proxy_async();
@@ -393,9 +462,20 @@ struct Pipe {
     }
 
     // Keep the Q0 ring full: prefetch element blocks ahead of the enumerate node.
+    // all queue positions start at `pos` (in-place rings share one coordinate system)
+    template <int e = 0>
+    __device__ __forceinline__ void start_at(uint32_t pos) {
+        if constexpr (e <= K) {
+            if (e == 0 || INPLACE) { E<e>().qh = E<e>().qt = pos; q_start[e] = pos; }
+            start_at<e + 1>(pos);
+        }
+    }
+    // oldest live ring position: in-place, the last data queue lies behind all others
+    __device__ __forceinline__ uint32_t oldest() const { return INPLACE ? E<NQ>().qh : E<0>().qh; }
+
     __device__ __forceinline__ void refill() {
         for (;;) {
-            if ((stg_j + 1) * sblk > E<0>().qh + ring0) return;   // ring slots still in use
+            if ((stg_j + 1) * sblk > oldest() + ring0) return;   // ring slots still in use
             const uint32_t sp = stg_j * sblk;
             if (F0.k >= 0 && sp < F0.pos + flen(F0)) { issue_stage(F0); continue; }
             if (F1.k >= 0 && sp < F1.pos + flen(F1)) { issue_stage(F1); continue; }
@@ -404,7 +484,7 @@ struct Pipe {
             if (k < 0) { claims_done = true; return; }
             if (F0.k < 0) {
                 const uint32_t pos = (k == 0) ? (uint32_t)(off0 - base0) : sp;
-                if (k == 0 && stg_j == 0) { E<0>().qh = E<0>().qt = pos; q_start[0] = pos; }
+                if (k == 0 && stg_j == 0) start_at(pos);
                 load_chunk(F0, k, pos);
                 pidx = 0;
                 begun = false;
@@ -613,7 +693,7 @@ struct Pipe {
 
     // ---------------------------------------------------------- stages
     __device__ __forceinline__ uint32_t landed_pos() {
-        while (landed_j < stg_j && mbar_test_uniform(&bar[landed_j % NST], (landed_j / NST) & 1u)) landed_j++;
+        while (landed_j < stg_j && mbar_test_uniform(&bar[landed_j & (nstg - 1)], (landed_j >> nsh) & 1u)) landed_j++;
         return landed_j * sblk;
     }
 
@@ -633,7 +713,7 @@ struct Pipe {
     template <int n, class Op>
     __device__ __forceinline__ void filter_full(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                                 uint32_t nens, const Op op) {
-        const uint32_t tl = filter_batch<TAG, Op, U8 && n == 1>(in, tin, imask, h, nens, Q<n>(), T<n>(), qmask,
+        const uint32_t tl = filter_batch<TAG, Op, U8 && n == 1>(in, tin, imask, h, nens, Q<n>(), T<n>(), qm<n>(),
                                                                E<n>().qt, op, lt, P.C - 1);
         E<n>().sent += tl - E<n>().qt;
         E<n>().qt = tl;
@@ -773,7 +853,7 @@ struct Pipe {
     __device__ __forceinline__ bool fire(bool drained) {
         constexpr int ei = n - 1;          // input edge
         constexpr bool AGGN = (n == K + 1) || (NA && n == K);   // node n performs the aggregate's actions
-        const uint32_t imask = (ei == 0) ? (ring0 - 1) : qmask;
+        const uint32_t imask = qm<ei>();
         const uint32_t *in = Q<ei>();
         const uint32_t *tin = T<ei>();
         bool prog = false;
@@ -790,7 +870,7 @@ struct Pipe {
                 ar = rdy <= 0 ? 0u : min(ar, (uint32_t)rdy);
             }
             uint32_t space = 0xffffffffu;
-            if constexpr (!AGGN) space = qcap - (E<n>().qt - E<n>().qh);
+            if constexpr (!AGGN && !INPLACE) space = qcap - (E<n>().qt - E<n>().qh);   // in-place: implied
             const uint32_t lim = min(ar, space);
             if (lim >= (uint32_t)W) {
                 // as many full ensembles as the credit / data / space allow
@@ -897,7 +977,7 @@ struct Pipe {
             }
         } else {
             const uint32_t tl = partial_stage<TAG, U8 && n == 1>(&P.st[n - 1], in, tin, imask, h, e, Q<n>(), T<n>(),
-                                                                qmask, E<n>().qt, lt, P.C - 1);
+                                                                qm<n>(), E<n>().qt, lt, P.C - 1);
             E<n>().sent += tl - E<n>().qt;
             E<n>().qt = tl;
         }
@@ -969,6 +1049,26 @@ struct Pipe {
         }
     }
 
+    // In-place rings: close the dead space left by filtered-out items -- move
+    // the (normally < w) items left in Q_e up to end right behind its
+    // producer's read head h_{e-1}, nearest to Q0 first.  Queue contents and
+    // counts are unchanged (credits and signal positions are counts), only the
+    // ring coordinates of Q_e shift, which frees its old slots for the TMA.
+    template <int e = 1>
+    __device__ __forceinline__ void relocate() {
+        if constexpr (INPLACE && e <= NQ) {
+            const uint32_t shift = E<e - 1>().qh - E<e>().qt;
+            if (shift != 0) {
+                const uint32_t n = E<e>().qt - E<e>().qh;
+                if (n != 0) move_items<TAG>(Q<0>(), T<0>(), E<e>().qt, n, shift, ring0 - 1);
+                E<e>().qh += shift;
+                E<e>().qt += shift;
+                q_start[e] += shift;
+            }
+            relocate<e + 1>();
+        }
+    }
+
     template <int n>
     __device__ __forceinline__ bool fire_chain(bool drained) {
         if constexpr (n > (NA ? K : K + 1)) {
@@ -989,7 +1089,7 @@ struct Pipe {
         if constexpr (n <= K + 1) {
             if (lane == 0) {
                 // c[0] = partial ensembles, c[1] = their items (accumulated in the run)
-                uint32_t *c = reinterpret_cast<uint32_t *>(base + 32) + 4 * n;
+                uint32_t *c = reinterpret_cast<uint32_t *>(base + CNT_OFF) + 4 * n;
                 const uint32_t items = E<n - 1>().qh - q_start[n - 1];
                 const uint32_t full = (items - c[1]) / W;
                 c[0] += full;
@@ -1015,7 +1115,7 @@ struct Pipe {
         finish_counters<1>(fitems);
         __syncwarp();
         if (lane < K + 2) {
-            const uint32_t *c = reinterpret_cast<const uint32_t *>(base + 32) + 4 * lane;
+            const uint32_t *c = reinterpret_cast<const uint32_t *>(base + CNT_OFF) + 4 * lane;
             unsigned long long *S = P.stats + 4 * lane;
 #pragma unroll
             for (int f = 0; f < 4; ++f)
@@ -1025,7 +1125,7 @@ struct Pipe {
 
     __device__ __forceinline__ void run() {
         if (lane == 0)
-            for (int i = 0; i < NST; ++i) mbar_init(&bar[i], 1);
+            for (uint32_t i = 0; i < nstg; ++i) mbar_init(&bar[i], 1);
         mbar_fence_init();
         __syncwarp();
         uint32_t idle = 0;
@@ -1035,12 +1135,14 @@ struct Pipe {
             if (prof) { pcnt(0, clock64() - t0); pcnt(8, 1); }
             prog |= fire_chain<1>(enum_done);
             if (enum_done && all_empty()) break;
+            if constexpr (INPLACE && NQ > 0)
+                if (E<0>().qh - oldest() >= (ring0 >> 2)) relocate();
             if (prog) { idle = 0; continue; }
             // nothing fireable: wait for the oldest in-flight TMA stage
             if (landed_j < stg_j) {
                 const long long tw = prof ? clock64() : 0;
                 uint32_t spins = 0;
-                while (!mbar_try_wait_uniform(&bar[landed_j % NST], (landed_j / NST) & 1u)) {
+                while (!mbar_try_wait_uniform(&bar[landed_j & (nstg - 1)], (landed_j >> nsh) & 1u)) {
                     if (++spins > (1u << 24)) break;
                 }
                 if (spins > (1u << 24)) {
@@ -1058,14 +1160,14 @@ struct Pipe {
         if constexpr (TAG) flush_tagged();
         // drain outstanding TMA stages before the CTA's shared memory is released
         for (uint32_t spins = 0; landed_j < stg_j && spins < (1u << 26); ++spins) {
-            if (mbar_try_wait_uniform(&bar[landed_j % NST], (landed_j / NST) & 1u)) landed_j++;
+            if (mbar_try_wait_uniform(&bar[landed_j & (nstg - 1)], (landed_j >> nsh) & 1u)) landed_j++;
         }
         __syncwarp();
         if (P.flags & RS_FLAG_STATS) flush_stats();
         if (prof && lane == 0) {
             // per-node cycles (enumerate, nodes 1..K+1, TMA wait), sweeps, waits
             unsigned long long *Pr = P.stats + 4 * (MAXK + 2);
-            const unsigned long long *c = reinterpret_cast<const unsigned long long *>(base + 128);
+            const unsigned long long *c = reinterpret_cast<const unsigned long long *>(base + PROF_OFF);
             for (int i = 0; i < 10; ++i) atomicAdd(Pr + i, c[i]);
             atomicAdd(Pr + 10, 1ull);
         }
@@ -1078,7 +1180,7 @@ __global__ void __launch_bounds__(WPB * 32, 4) k_pipeline(const __grid_constant_
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     using PP = Pipe<K, AGG, TAG, FUSE>;
-    uint8_t *mine = smem + (size_t)warp * PP::smem_bytes(P.qcap, P.scap, P.q0_stage);
+    uint8_t *mine = smem + (size_t)warp * PP::smem_bytes(P.qcap, P.scap, P.ring0);
     if (P.hdr->err) return;
     PP pipe(P, mine, lane);
     pipe.run();

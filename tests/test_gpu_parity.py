@@ -121,7 +121,8 @@ def test_random_parity(rs, seed, strategy, mode):
     vals, off, stages = _case(seed, agg)
     rnd = random.Random(seed * 7 + 1)
     cfg = dict(chunk=rnd.choice([2048, 4096, 8192]), grid=rnd.choice([0, 0, 1, 3]),
-               queue_cap=rnd.choice([256, 512]), signal_cap=rnd.choice([4, 16, 128]))
+               queue_cap=rnd.choice([256, 512]), signal_cap=rnd.choice([4, 16, 128]),
+               q0_stage=rnd.choice([0, 128, 256]))   # in-place rings down to 512 items (heavy relocation)
     ref = oracle.brute(vals, off, stages, agg)
     got, st, _ = run_gpu(rs, vals, off, stages, agg, strategy, mode, **cfg)
     assert_parity(got, ref, agg)
@@ -199,9 +200,12 @@ def test_grid_and_capacity_invariance(rs):
     stages = synth.sweep_stages(3)
     ref = oracle.brute(vals, off, stages, "sum_i64")
     for cfg in (dict(grid=1), dict(grid=2, chunk=2048), dict(queue_cap=1024, signal_cap=8), dict(signal_cap=4),
-                dict(queue_cap=256)):
+                dict(queue_cap=256), dict(q0_stage=128, queue_cap=256), dict(q0_stage=128, queue_cap=1024),
+                dict(q0_stage=2048, queue_cap=16384, chunk=2048)):
         for strat in ("signal", "tagged"):
             for mode in ("ws", "seq", "unfused"):
+                if mode == "ws" and "q0_stage" in cfg:
+                    continue                 # in-place ring sizes are a sequential-kernel knob
                 got, _, _ = run_gpu(rs, vals, off, stages, "sum_i64", strat, mode, **cfg)
                 assert_parity(got, ref, "sum_i64")
 
