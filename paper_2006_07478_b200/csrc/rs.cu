@@ -156,7 +156,7 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     const bool inplace = elem != RS_U8 && !(cfg.flags & RS_FLAG_WARP_SPECIALIZED);
     const bool tagged_ = cfg.strategy == RS_STRATEGY_TAGGED;
     if (cfg.queue_cap == 0) cfg.queue_cap = inplace ? (tagged_ ? 16 * W : 32 * W) : (nst_ >= 2 ? 8 * W : 16 * W);
-    if (cfg.signal_cap == 0) cfg.signal_cap = nst_ >= 2 ? 64 : 128;
+    if (cfg.signal_cap == 0) cfg.signal_cap = inplace ? 32 : (nst_ >= 2 ? 64 : 128);
     if (cfg.q0_stage == 0)
         cfg.q0_stage = inplace ? (tagged_ ? 512 : 1024) : ((tagged_ || nst_ >= 2) ? 256 : 512);
     if (!is_pow2(cfg.queue_cap) || cfg.queue_cap < 2 * W || cfg.queue_cap > 65536)
@@ -251,7 +251,7 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
             // sequential scheduler: one instance per warp; pick warps-per-CTA to
             // pack the most instances per SM
             int best = 0, best_w = 1;
-            for (int w = WPB; w >= 1; w >>= 1) {
+            for (int w = WPB_MAX; w >= 1; --w) {
                 const uint32_t bytes = L.inst_bytes * w;
                 if (cudaFuncSetAttribute(L.main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
                     cudaGetLastError();

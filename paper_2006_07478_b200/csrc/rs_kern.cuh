@@ -41,7 +41,8 @@ constexpr uint32_t END_BIT = 0x80000000u;  // signal word: kind End
 constexpr int MAXK = 4;             // max FILTER/TRANSFORM stages
 constexpr int NST = 4;              // TMA stages in the Q0 ring (warp-specialised kernel; separate-queue rings)
 constexpr int NSTMAX = 8;           // TMA stages of an in-place ring (sequential kernel)
-constexpr int WPB = 4;              // warps (instances) per CTA
+constexpr int WPB = 4;              // warps (instances) per CTA (default)
+constexpr int WPB_MAX = 16;         // sequential kernel: up to 16 instances per CTA (one CTA may fill an SM)
 
 enum : int32_t { ERR_OFFSETS = 1, ERR_WATCHDOG = 2, ERR_SIGFULL = 3, ERR_UNMATCHED = 4, ERR_QFULL = 5, ERR_LIMIT = 7 };
 

@@ -1175,7 +1175,7 @@ struct Pipe {
 };
 
 template <int K, int AGG, bool TAG, bool FUSE>
-__global__ void __launch_bounds__(WPB * 32, 4) k_pipeline(const __grid_constant__ KParams P) {
+__global__ void __launch_bounds__(WPB_MAX * 32, 1) k_pipeline(const __grid_constant__ KParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
