@@ -102,14 +102,17 @@ __device__ __noinline__ uint32_t filter_batch(const uint32_t *in, const uint32_t
 }
 
 // One partial ensemble (e < w items: signal-bounded or the drained tail) of
-// a FILTER/TRANSFORM node; shared by every stage node (code size).
-template <bool TAG, bool U8IN>
-__device__ __noinline__ uint32_t partial_stage(const StageP *sp, const uint32_t *in, const uint32_t *tin,
+// a FILTER/TRANSFORM node, specialised per op like the full ensembles and
+// shared by every stage node (code size); only the ceil(e/32) occupied
+// slices are visited (e is warp-uniform).
+template <bool TAG, class Op, bool U8IN>
+__device__ __noinline__ uint32_t partial_stage(const Op op, const uint32_t *in, const uint32_t *tin,
                                                uint32_t imask, uint32_t h, uint32_t e, uint32_t *out, uint32_t *tout,
                                                uint32_t qmask, uint32_t tl, uint32_t lt, uint32_t cmask) {
     const uint32_t lane = threadIdx.x & 31u;
 #pragma unroll
     for (int j = 0; j < IPL; ++j) {
+        if ((uint32_t)j * 32u >= e) break;
         const uint32_t idx = j * 32 + lane;
         const bool act = idx < e;
         uint32_t v = act ? load_item<U8IN>(in, h + idx, imask, cmask) : 0u;
@@ -118,7 +121,7 @@ __device__ __noinline__ uint32_t partial_stage(const StageP *sp, const uint32_t 
             tg = act ? tin[(h + idx) & imask] : 0u;
             __syncwarp();   // in-place rings: tag reads precede the tag stores
         }
-        const bool keep = act && stage_apply(*sp, v);
+        const bool keep = act && op(v);
         const uint32_t mk = __ballot_sync(kFull, keep);   // stable compaction
         if (keep) {
             const uint32_t pos = (tl + __popc(mk & lt)) & qmask;
@@ -129,6 +132,25 @@ __device__ __noinline__ uint32_t partial_stage(const StageP *sp, const uint32_t 
     }
     __syncwarp();
     return tl;
+}
+
+// Calls f(op) with the node's op as its specialised functor (one switch per
+// firing instead of one per item).
+template <class F>
+__device__ __forceinline__ void with_op(const StageP &sp, F &&f) {
+    switch (sp.op) {
+        case RS_OP_HASH_LT:
+            if (sp.b >= 256) f(OpAll{});
+            else f(OpHash{sp.a, sp.b << 24});
+            break;
+        case RS_OP_LT_U32:
+            if (sp.table[0]) f(OpAll{});
+            else f(OpLt{sp.b, false});
+            break;
+        case RS_OP_CLASS: f(OpClass{sp.table}); break;
+        case RS_OP_SCALE_F32: f(OpScale{__uint_as_float(sp.a)}); break;
+        default: f(OpAffine{sp.a, sp.b}); break;
+    }
 }
 
 // Fused terminal node, full ensembles, signal strategy (see Pipe::FUSE): the
@@ -225,6 +247,36 @@ __device__ __noinline__ void move_items(uint32_t *q, uint32_t *tq, uint32_t end,
         end -= c;
         n -= c;
     }
+}
+
+// Fused node K, one partial ensemble (signal strategy): op + fold of the
+// occupied slices only.
+template <class AT, class Op, bool U8IN>
+__device__ __noinline__ FusedAcc<AT> fused_partial(const uint32_t *in, uint32_t imask, uint32_t h, uint32_t e,
+                                                   const Op op, long long adelta, uint32_t cmask, FusedAcc<AT> st) {
+    const uint32_t lane = threadIdx.x & 31u;
+    if constexpr (AT::heavy) {
+        uint32_t v[IPL], km = 0;
+#pragma unroll
+        for (int j = 0; j < IPL; ++j) {
+            const uint32_t idx = j * 32 + lane;
+            v[j] = idx < e ? load_item<U8IN>(in, h + idx, imask, cmask) : 0u;
+            km |= (idx < e && op(v[j])) ? 1u << j : 0u;
+        }
+        st.kept += __popc(km);
+        st.acc = fold_kept<AT>(st.acc, v, km, adelta);
+    } else {
+#pragma unroll
+        for (int j = 0; j < IPL; ++j) {
+            if ((uint32_t)j * 32u >= e) break;
+            const uint32_t idx = j * 32 + lane;
+            uint32_t v = idx < e ? load_item<U8IN>(in, h + idx, imask, cmask) : 0u;
+            const bool keep = idx < e && op(v);
+            st.kept += keep ? 1u : 0u;
+            if (keep) st.acc = AT::comb(st.acc, AT::lift_i(v, adelta));
+        }
+    }
+    return st;
 }
 
 struct Chunk {
@@ -951,33 +1003,21 @@ struct Pipe {
             }
         } else if constexpr (NA && n == K) {
             if constexpr (!TAG) {
-                const OpDyn op{&P.st[n - 1]};
-                if constexpr (AT::heavy) {
-                    uint32_t v[IPL], km = 0;
-#pragma unroll
-                    for (int j = 0; j < IPL; ++j) {
-                        const uint32_t idx = j * 32 + lane;
-                        v[j] = idx < e ? agg_load(in, h + idx, imask) : 0u;
-                        km |= (idx < e && op(v[j])) ? 1u << j : 0u;
-                    }
-                    fkept += __popc(km);
-                    acc = fold_kept<AT>(acc, v, km, adelta);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < IPL; ++j) {
-                        const uint32_t idx = j * 32 + lane;
-                        uint32_t v = idx < e ? agg_load(in, h + idx, imask) : 0u;
-                        const bool keep = idx < e && op(v);
-                        fkept += keep ? 1u : 0u;
-                        if (keep) acc = AT::comb(acc, AT::lift_i(v, adelta));
-                    }
-                }
+                with_op(P.st[n - 1], [&](auto op) {
+                    const FusedAcc<AT> r = fused_partial<AT, decltype(op), AGG_U8IN>(in, imask, h, e, op, adelta, P.C - 1,
+                                                                                     FusedAcc<AT>{acc, fkept});
+                    acc = r.acc;
+                    fkept = r.kept;
+                });
             } else {
                 agg_tagged(in, tin, imask, h, e, OpDyn{&P.st[n - 1]});
             }
         } else {
-            const uint32_t tl = partial_stage<TAG, U8 && n == 1>(&P.st[n - 1], in, tin, imask, h, e, Q<n>(), T<n>(),
-                                                                qm<n>(), E<n>().qt, lt, P.C - 1);
+            uint32_t tl = E<n>().qt;
+            with_op(P.st[n - 1], [&](auto op) {
+                tl = partial_stage<TAG, decltype(op), U8 && n == 1>(op, in, tin, imask, h, e, Q<n>(), T<n>(), qm<n>(),
+                                                                    tl, lt, P.C - 1);
+            });
             E<n>().sent += tl - E<n>().qt;
             E<n>().qt = tl;
         }
