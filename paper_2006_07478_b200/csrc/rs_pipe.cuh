@@ -949,34 +949,44 @@ struct Pipe {
                 prog = true;
                 continue;
             }
-            // signal phase: only with the counter at 0
+            // signal phase: only with the counter at 0.  Back-to-back
+            // signals (credit 0, A4) are consumed in one pass; the first later
+            // signal with a positive credit moves it into the counter (rule 2b)
+            // so the next data phase starts without re-reading the queue.
             if constexpr (TAG) break;
             if (!spend || E<ei>().cur != 0) break;
-            const uint2 hs = S<ei>()[E<ei>().sh & smask];
-            if (!E<ei>().xfer && (hs.y & ~END_BIT) > 0) {
-                E<ei>().cur = hs.y & ~END_BIT;
-                E<ei>().xfer = true;
-                continue;
-            }
-            if constexpr (!AGGN) {
-                if (scap - (E<n>().st - E<n>().sh) == 0) break;
-            }
-            E<ei>().sh++;
-            E<ei>().xfer = false;
-            prog = true;
-            const bool is_end = (hs.y & END_BIT) != 0;
-            if constexpr (AGGN) {
-                if (!is_end) {               // a::begin: acc = identity
-                    acc = AT::id();
-                    if constexpr (U8) adelta = part_delta(hs.x);
-                } else {                     // a::end: push(acc)
-                    const A v = warp_reduce<AT>(acc);
-                    if (lane == 0) store_key(hs.x, v);
-                    acc = AT::id();
+            uint32_t nsig = 0;
+            for (;;) {
+                if constexpr (!AGGN) {
+                    if (scap - (E<n>().st - E<n>().sh) == 0) break;   // output signal queue full
                 }
-            } else {
-                push_signal<n>(hs.x, is_end, E<n>().sent);   // forwarded with a fresh credit
+                const uint2 hs = S<ei>()[E<ei>().sh & smask];
+                E<ei>().sh++;
+                E<ei>().xfer = false;
+                ++nsig;
+                const bool is_end = (hs.y & END_BIT) != 0;
+                if constexpr (AGGN) {
+                    if (!is_end) {               // a::begin: acc = identity
+                        acc = AT::id();
+                        if constexpr (U8) adelta = part_delta(hs.x);
+                    } else {                     // a::end: push(acc)
+                        const A v = warp_reduce<AT>(acc);
+                        if (lane == 0) store_key(hs.x, v);
+                        acc = AT::id();
+                    }
+                } else {
+                    push_signal<n>(hs.x, is_end, E<n>().sent);   // forwarded with a fresh credit
+                }
+                if (E<ei>().sh == E<ei>().st) break;
+                const uint32_t c = S<ei>()[E<ei>().sh & smask].y & ~END_BIT;
+                if (c > 0) {
+                    E<ei>().cur = c;
+                    E<ei>().xfer = true;
+                    break;
+                }
             }
+            if (nsig == 0) break;
+            prog = true;
         }
         __syncwarp();
         return prog;
