@@ -923,38 +923,41 @@ struct Pipe {
             }
             uint32_t space = 0xffffffffu;
             if constexpr (!AGGN && !INPLACE) space = qcap - (E<n>().qt - E<n>().qh);   // in-place: implied
-            const uint32_t lim = min(ar, space);
+            uint32_t lim = min(ar, space);
+            uint32_t arem = a;
+            bool did = false;
             if (lim >= (uint32_t)W) {
                 // as many full ensembles as the credit / data / space allow
                 const uint32_t nens = lim / W;
                 run_full<n>(in, tin, imask, E<ei>().qh, nens);
                 E<ei>().qh += nens * W;
                 if (spend) E<ei>().cur -= nens * W;
-                prog = true;
-                continue;
+                lim -= nens * W;
+                arem -= nens * W;
+                did = true;
             }
-            const uint32_t e = lim;
-            bool ok = e > 0;
-            if (ok) {
-                const bool bounded = spend && e == E<ei>().cur;        // ensemble <= credit
-                const bool dr = drained && e == a;
-                ok = bounded || dr;
-            }
-            if (ok) {
-                run_partial<n>(in, tin, imask, E<ei>().qh, e);
-                E<ei>().qh += e;
-                if (spend) E<ei>().cur -= e;
-                stat_add(n, 0, 1u);            // partial ensembles and their items; full
-                stat_add(n, 1, e);             // ensembles are derived at exit
-                prog = true;
-                continue;
+            // then at most one partial ensemble, in the same pass
+            if (lim > 0) {
+                const bool bounded = spend && lim == E<ei>().cur;      // ensemble <= credit
+                const bool dr = drained && lim == arem;
+                if (bounded || dr) {
+                    run_partial<n>(in, tin, imask, E<ei>().qh, lim);
+                    E<ei>().qh += lim;
+                    if (spend) E<ei>().cur -= lim;
+                    stat_add(n, 0, 1u);            // partial ensembles and their items; full
+                    stat_add(n, 1, lim);           // ensembles are derived at exit
+                    did = true;
+                }
             }
             // signal phase: only with the counter at 0.  Back-to-back
             // signals (credit 0, A4) are consumed in one pass; the first later
             // signal with a positive credit moves it into the counter (rule 2b)
             // so the next data phase starts without re-reading the queue.
-            if constexpr (TAG) break;
-            if (!spend || E<ei>().cur != 0) break;
+            if (TAG || !spend || E<ei>().cur != 0) {
+                if (!did) break;
+                prog = true;
+                continue;
+            }
             uint32_t nsig = 0;
             for (;;) {
                 if constexpr (!AGGN) {
@@ -985,7 +988,7 @@ struct Pipe {
                     break;
                 }
             }
-            if (nsig == 0) break;
+            if (nsig == 0 && !did) break;
             prog = true;
         }
         __syncwarp();
