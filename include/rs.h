@@ -83,7 +83,12 @@ typedef enum { RS_I32 = 0, RS_U32 = 1, RS_U8 = 2, RS_F32 = 3 } rs_dtype;
 
 typedef enum {
     RS_STRATEGY_SIGNAL = 0,  /* Begin/End signals with credits (§3, §4.2)  */
-    RS_STRATEGY_TAGGED = 1   /* per-item region tags          */
+    RS_STRATEGY_TAGGED = 1,  /* per-item region tags          */
+    RS_STRATEGY_AUTO = 2     /* choice made per run, transparently (§8 f1):
+                                signal when the mean region length n_elems / n_regions is at
+                                least cfg.auto_min_len, else tagged.  Both strategies give
+                                bit-identical integer aggregates, so the choice only
+                                moves time.  rs_pipeline_last_strategy reports it. */
 } rs_strategy;
 
 typedef struct {
@@ -128,6 +133,9 @@ typedef struct {
                                 stages); power of 2 in [128, 4096], <= chunk; 0 = auto (in-place
                                 rings: 1024 signal, 512 tagged; otherwise 256 tagged or 2+ stages,
                                 else 512) */
+    uint32_t auto_min_len;   /* RS_STRATEGY_AUTO: mean children per region at and above which the
+                                signal strategy runs; 0 = the crossover measured on B200 for the
+                                pipeline's stage count */
 } rs_config;
 
 /* Per-node occupancy counters (§2.2, §5).  Node 0 is the
@@ -212,6 +220,10 @@ int rs_pipeline_launches(const rs_pipeline *p);
 /* Persistent CTAs and warps (pipeline instances) per CTA of the last run. */
 rs_status rs_pipeline_geometry(const rs_pipeline *p, int32_t *grid, int32_t *warps_per_cta,
                                int32_t *chunk);
+
+/* Strategy the last run used (RS_STRATEGY_SIGNAL or RS_STRATEGY_TAGGED; for an
+ * AUTO pipeline that has not run yet, RS_STRATEGY_AUTO).  Host only. */
+rs_status rs_pipeline_last_strategy(const rs_pipeline *p, int32_t *strategy);
 
 void rs_pipeline_destroy(rs_pipeline *p);
 

@@ -23,13 +23,14 @@ RS_NODE_ENUMERATE, RS_NODE_FILTER, RS_NODE_TRANSFORM, RS_NODE_AGGREGATE = 1, 2, 
 OPS = {"none": 0, "hash_lt": 1, "lt_u32": 2, "class": 3, "scale_f32": 10, "affine_i32": 11,
        "sum_i64": 20, "sum_f32": 21, "count_min_u32": 22, "count_xor64": 23}
 DTYPES = {"i32": 0, "u32": 1, "u8": 2, "f32": 3}
-STRATEGIES = {"signal": 0, "tagged": 1}
+STRATEGIES = {"signal": 0, "tagged": 1, "auto": 2}
+STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
 RS_FLAG_STATS, RS_FLAG_VALIDATE, RS_FLAG_TIMING, RS_FLAG_WARP_SPECIALIZED, RS_FLAG_PROFILE, RS_FLAG_UNFUSED = 1, 2, 4, 8, 16, 32
 
 EXPORTS = ["rs_config_default", "rs_pipeline_create", "rs_pipeline_workspace_bytes", "rs_pipeline_run",
            "rs_pipeline_run_host", "rs_pipeline_stats", "rs_pipeline_profile", "rs_pipeline_check",
            "rs_pipeline_kernel_times",
-           "rs_pipeline_launches",
+           "rs_pipeline_launches", "rs_pipeline_last_strategy",
            "rs_pipeline_geometry", "rs_pipeline_destroy", "rs_status_string", "rs_last_error"]
 
 
@@ -47,7 +48,7 @@ class rs_node(C.Structure):
 class rs_config(C.Structure):
     _fields_ = [("strategy", C.c_int32), ("simd_width", C.c_uint32), ("queue_cap", C.c_uint32),
                 ("signal_cap", C.c_uint32), ("grid", C.c_int32), ("chunk", C.c_uint32),
-                ("flags", C.c_uint32), ("q0_stage", C.c_uint32)]
+                ("flags", C.c_uint32), ("q0_stage", C.c_uint32), ("auto_min_len", C.c_uint32)]
 
 
 class rs_node_stats(C.Structure):
@@ -83,6 +84,7 @@ def lib():
         L.rs_pipeline_kernel_times.restype = i32
         L.rs_pipeline_launches.argtypes = [vp]
         L.rs_pipeline_launches.restype = i32
+        L.rs_pipeline_last_strategy.argtypes = [vp, C.POINTER(C.c_int32)]
         L.rs_pipeline_geometry.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         L.rs_pipeline_destroy.argtypes = [vp]
         L.rs_pipeline_destroy.restype = None
@@ -90,7 +92,8 @@ def lib():
         L.rs_status_string.restype = C.c_char_p
         L.rs_last_error.restype = C.c_char_p
         for name in ("rs_config_default", "rs_pipeline_create", "rs_pipeline_workspace_bytes", "rs_pipeline_run",
-                     "rs_pipeline_run_host", "rs_pipeline_stats", "rs_pipeline_check", "rs_pipeline_geometry"):
+                     "rs_pipeline_run_host", "rs_pipeline_stats", "rs_pipeline_check", "rs_pipeline_geometry",
+                     "rs_pipeline_last_strategy"):
             getattr(L, name).restype = i32
         _lib = L
     return _lib
@@ -129,7 +132,7 @@ class Pipeline:
     ``agg``: aggregate op name.  Node list = [ENUMERATE] + stages + [AGGREGATE]."""
 
     def __init__(self, stages, agg, elem=None, strategy="signal", queue_cap=0, signal_cap=0, grid=0,
-                 chunk=0, flags=RS_FLAG_STATS, simd_width=128, q0_stage=0):
+                 chunk=0, flags=RS_FLAG_STATS, simd_width=128, q0_stage=0, auto_min_len=0):
         L = lib()
         self.stages = list(stages)
         self.agg = agg
@@ -158,6 +161,7 @@ class Pipeline:
         cfg.chunk = chunk
         cfg.flags = flags
         cfg.q0_stage = q0_stage
+        cfg.auto_min_len = auto_min_len
         h = C.c_void_p()
         _check(L.rs_pipeline_create(nodes, len(self.stages) + 2, DTYPES[self.elem], C.byref(cfg), C.byref(h)))
         self.h = h
@@ -174,6 +178,12 @@ class Pipeline:
             self.close()
         except Exception:
             pass
+
+    def last_strategy(self) -> str:
+        """Strategy the last run used ("signal"/"tagged"; "auto" before the first run)."""
+        v = C.c_int32()
+        _check(lib().rs_pipeline_last_strategy(self.h, C.byref(v)))
+        return STRATEGY_NAMES[v.value]
 
     def workspace_bytes(self, n_regions: int, n_elems: int) -> int:
         b = C.c_size_t()

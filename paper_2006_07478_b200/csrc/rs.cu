@@ -44,9 +44,35 @@ struct rs_pipeline {
     // run_host buffers
     void *h_dbuf = nullptr;
     size_t h_dbuf_bytes = 0;
+    // RS_STRATEGY_AUTO: one pipeline per strategy, the run picks (§8 f1)
+    rs_pipeline *sub[2] = {nullptr, nullptr};
+    rs_pipeline *last = nullptr;
+    uint32_t auto_min_len = 0;
 };
 
 namespace {
+
+// AUTO pipelines: the sub-pipeline a run uses (mean region length vs the
+// crossover), and the one queries refer to (the last run's).
+rs_pipeline *choose(rs_pipeline *p, int64_t n_elems, int64_t n_regions) {
+    if (!p->sub[0]) return p;
+    const bool sig = n_regions > 0 && (double)n_elems >= (double)p->auto_min_len * (double)n_regions;
+    p->last = p->sub[sig ? 0 : 1];
+    return p->last;
+}
+const rs_pipeline *route(const rs_pipeline *p) {
+    if (!p || !p->sub[0]) return p;
+    return p->last ? p->last : p->sub[0];
+}
+rs_pipeline *route(rs_pipeline *p) { return const_cast<rs_pipeline *>(route(static_cast<const rs_pipeline *>(p))); }
+
+// Crossover region length (children per region) above which the signal
+// strategy beats tagged on B200, by FILTER/TRANSFORM stage count
+// (tools/crossover.py).
+uint32_t auto_default(int nst) {
+    static const uint32_t T[MAXK + 1] = {AUTO_T0, AUTO_T1, AUTO_T2, AUTO_T3, AUTO_T4};
+    return T[nst < 0 ? 0 : (nst > MAXK ? MAXK : nst)];
+}
 
 bool get_launch(const rs_pipeline *p, Launch *L) {
     switch (p->agg) {
@@ -108,6 +134,7 @@ rs_status rs_config_default(rs_config *cfg) {
     cfg->chunk = 0;
     cfg->flags = RS_FLAG_STATS;
     cfg->q0_stage = 0;
+    cfg->auto_min_len = 0;
     return RS_OK;
 }
 
@@ -140,6 +167,29 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
                 return fail(RS_ERR_UNSUPPORTED, "COUNT_XOR64 is built for the sequential scheduler only");
             break;
         default: return fail(RS_ERR_UNSUPPORTED, "unknown aggregate op");
+    }
+    if (cfg.strategy == RS_STRATEGY_AUTO) {
+        rs_config c = cfg;
+        rs_pipeline *a = nullptr, *b = nullptr;
+        c.strategy = RS_STRATEGY_SIGNAL;
+        rs_status s = rs_pipeline_create(nodes, n_nodes, elem, &c, &a);
+        if (s != RS_OK) return s;
+        c.strategy = RS_STRATEGY_TAGGED;
+        s = rs_pipeline_create(nodes, n_nodes, elem, &c, &b);
+        if (s != RS_OK) { rs_pipeline_destroy(a); return s; }
+        rs_pipeline *p = new rs_pipeline();
+        p->cfg = a->cfg;
+        p->cfg.strategy = RS_STRATEGY_AUTO;
+        p->elem = elem;
+        p->n_nodes = n_nodes;
+        p->nst = nst;
+        p->agg = agg;
+        std::memcpy(p->st, a->st, sizeof p->st);
+        p->sub[0] = a;
+        p->sub[1] = b;
+        p->auto_min_len = cfg.auto_min_len ? cfg.auto_min_len : auto_default(nst);
+        *out = p;
+        return RS_OK;
     }
     if (cfg.strategy != RS_STRATEGY_SIGNAL && cfg.strategy != RS_STRATEGY_TAGGED)
         return fail(RS_ERR_INVALID_ARG, "bad strategy");
@@ -217,6 +267,13 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
 rs_status rs_pipeline_workspace_bytes(const rs_pipeline *p, int64_t n_regions, int64_t n_elems, size_t *bytes) {
     if (!p || !bytes) return fail(RS_ERR_INVALID_ARG, "NULL argument");
     if (n_regions < 0 || n_elems < 0) return fail(RS_ERR_INVALID_ARG, "negative size");
+    if (p->sub[0]) {                      // AUTO: enough for either strategy
+        size_t a = 0, b = 0;
+        rs_status s = rs_pipeline_workspace_bytes(p->sub[0], n_regions, n_elems, &a);
+        if (s == RS_OK) s = rs_pipeline_workspace_bytes(p->sub[1], n_regions, n_elems, &b);
+        *bytes = a > b ? a : b;
+        return s;
+    }
     Launch L;
     if (!get_launch(p, &L)) return fail(RS_ERR_UNSUPPORTED, "aggregate not built");
     *bytes = layout(p, n_regions, n_elems, L).total;
@@ -329,7 +386,9 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
 
 rs_status rs_pipeline_run(rs_pipeline *p, const void *d_elems, int64_t n_elems, const int64_t *d_offsets,
                           int64_t n_regions, rs_aggregates out, void *d_ws, size_t ws_bytes, rs_stream stream) {
-    return run_impl(p, d_elems, n_elems, d_offsets, n_regions, out, d_ws, ws_bytes, (cudaStream_t)stream);
+    if (!p) return fail(RS_ERR_INVALID_ARG, "pipeline is NULL");
+    return run_impl(choose(p, n_elems, n_regions), d_elems, n_elems, d_offsets, n_regions, out, d_ws, ws_bytes,
+                    (cudaStream_t)stream);
 }
 
 rs_status rs_pipeline_run_host(rs_pipeline *p, const void *h_elems, int64_t n_elems, const int64_t *h_offsets,
@@ -338,6 +397,7 @@ rs_status rs_pipeline_run_host(rs_pipeline *p, const void *h_elems, int64_t n_el
     if (n_regions < 0 || n_elems < 0) return fail(RS_ERR_INVALID_ARG, "negative size");
     if (n_regions == 0) return RS_OK;
     if (!h_offsets || (n_elems > 0 && !h_elems)) return fail(RS_ERR_INVALID_ARG, "NULL host buffer");
+    if (p->sub[0]) return rs_pipeline_run_host(choose(p, n_elems, n_regions), h_elems, n_elems, h_offsets, n_regions, h_out, stream_);
     Launch L;
     if (!get_launch(p, &L)) return fail(RS_ERR_UNSUPPORTED, "aggregate not built");
     if (!h_out.v0 || (L.out_bytes1 && !h_out.v1)) return fail(RS_ERR_INVALID_ARG, "output array is NULL");
@@ -376,6 +436,7 @@ rs_status rs_pipeline_run_host(rs_pipeline *p, const void *h_elems, int64_t n_el
 }
 
 rs_status rs_pipeline_profile(rs_pipeline *p, uint64_t *host16, rs_stream stream) {
+    p = route(p);
     if (!p || !host16) return fail(RS_ERR_INVALID_ARG, "NULL argument");
     if (!p->last_ws) { std::memset(host16, 0, 16 * sizeof(uint64_t)); return RS_OK; }
     if (cudaMemcpyAsync(host16, (uint8_t *)p->last_ws + 256 + sizeof(unsigned long long) * 4 * (MAXK + 2),
@@ -386,6 +447,7 @@ rs_status rs_pipeline_profile(rs_pipeline *p, uint64_t *host16, rs_stream stream
 }
 
 rs_status rs_pipeline_stats(rs_pipeline *p, rs_node_stats *host_out, int n_nodes, rs_stream stream) {
+    p = route(p);
     if (!p || !host_out) return fail(RS_ERR_INVALID_ARG, "NULL argument");
     if (n_nodes != p->n_nodes) return fail(RS_ERR_INVALID_ARG, "n_nodes must equal the create-time node count");
     if (!p->last_ws) {
@@ -407,6 +469,7 @@ rs_status rs_pipeline_stats(rs_pipeline *p, rs_node_stats *host_out, int n_nodes
 }
 
 rs_status rs_pipeline_check(rs_pipeline *p, rs_stream stream, int32_t *code) {
+    p = route(p);
     if (!p) return fail(RS_ERR_INVALID_ARG, "NULL pipeline");
     if (code) *code = 0;
     if (!p->last_ws) return RS_OK;
@@ -419,9 +482,20 @@ rs_status rs_pipeline_check(rs_pipeline *p, rs_stream stream, int32_t *code) {
     return RS_OK;
 }
 
-int rs_pipeline_launches(const rs_pipeline *p) { return p ? p->launches : 0; }
+int rs_pipeline_launches(const rs_pipeline *p) {
+    p = route(p);
+    return p ? p->launches : 0;
+}
+
+rs_status rs_pipeline_last_strategy(const rs_pipeline *p, int32_t *strategy) {
+    if (!p || !strategy) return fail(RS_ERR_INVALID_ARG, "NULL argument");
+    if (p->sub[0]) *strategy = p->last ? p->last->cfg.strategy : RS_STRATEGY_AUTO;
+    else *strategy = p->cfg.strategy;
+    return RS_OK;
+}
 
 rs_status rs_pipeline_kernel_times(rs_pipeline *p, float *ms3, rs_stream stream) {
+    p = route(p);
     if (!p || !ms3) return fail(RS_ERR_INVALID_ARG, "NULL argument");
     if (!p->timed || !p->ev[0]) return fail(RS_ERR_INVALID_ARG, "last run was not made with RS_FLAG_TIMING");
     if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return fail(RS_ERR_CUDA, "stream synchronize failed");
@@ -431,6 +505,7 @@ rs_status rs_pipeline_kernel_times(rs_pipeline *p, float *ms3, rs_stream stream)
 }
 
 rs_status rs_pipeline_geometry(const rs_pipeline *p, int32_t *grid, int32_t *wpb, int32_t *chunk) {
+    p = route(p);
     if (!p) return fail(RS_ERR_INVALID_ARG, "NULL pipeline");
     if (grid) *grid = p->grid;
     if (wpb) *wpb = p->wpb;
@@ -440,6 +515,8 @@ rs_status rs_pipeline_geometry(const rs_pipeline *p, int32_t *grid, int32_t *wpb
 
 void rs_pipeline_destroy(rs_pipeline *p) {
     if (!p) return;
+    rs_pipeline_destroy(p->sub[0]);
+    rs_pipeline_destroy(p->sub[1]);
     if (p->h_dbuf) cudaFree(p->h_dbuf);
     for (int i = 0; i < 4; ++i)
         if (p->ev[i]) cudaEventDestroy(p->ev[i]);

@@ -39,6 +39,9 @@ constexpr int IPL = W / 32;         // items per lane per ensemble
 constexpr uint32_t SLOT = 0x80000000u;  // key bit: partial-aggregate slot instead of region id
 constexpr uint32_t END_BIT = 0x80000000u;  // signal word: kind End
 constexpr int MAXK = 4;             // max FILTER/TRANSFORM stages
+// RS_STRATEGY_AUTO crossover (children per region at which signal beats
+// tagged) by stage count 0..4, measured on B200 (tools/crossover.py)
+constexpr uint32_t AUTO_T0 = 128, AUTO_T1 = 256, AUTO_T2 = 512, AUTO_T3 = 768, AUTO_T4 = 2048;
 constexpr int NST = 4;              // TMA stages in the Q0 ring (warp-specialised kernel; separate-queue rings)
 constexpr int NSTMAX = 8;           // TMA stages of an in-place ring (sequential kernel)
 constexpr int WPB = 4;              // warps (instances) per CTA (default)

@@ -46,6 +46,7 @@ def test_enums_match_header(rs):
     assert val("RS_NODE_ENUMERATE") == rs.RS_NODE_ENUMERATE
     assert val("RS_NODE_AGGREGATE") == rs.RS_NODE_AGGREGATE
     assert val("RS_STRATEGY_TAGGED") == rs.STRATEGIES["tagged"]
+    assert val("RS_STRATEGY_AUTO") == rs.STRATEGIES["auto"]
     assert val("RS_F32") == rs.DTYPES["f32"]
     assert val("RS_ERR_PROTOCOL") == rs.RS_ERR_PROTOCOL
 
@@ -116,3 +117,16 @@ def test_binding_fails_loudly_without_library(rs, tmp_path, monkeypatch):
     monkeypatch.setattr(rs, "LIB_PATH", str(tmp_path / "missing.so"))
     with pytest.raises(ImportError):
         rs.lib()
+
+
+def test_auto_strategy_host_side(rs):
+    """RS_STRATEGY_AUTO creates on the host, reports AUTO before
+    any run, and sizes its workspace for either strategy (no GPU needed)."""
+    import synth
+    p = rs.Pipeline(synth.sweep_stages(3), "sum_i64", strategy="auto")
+    assert p.last_strategy() == "auto"
+    s = rs.Pipeline(synth.sweep_stages(3), "sum_i64", strategy="signal")
+    t = rs.Pipeline(synth.sweep_stages(3), "sum_i64", strategy="tagged")
+    for R, N in ((10, 1000), (1 << 20, 1 << 24)):
+        assert p.workspace_bytes(R, N) == max(s.workspace_bytes(R, N), t.workspace_bytes(R, N))
+    assert s.last_strategy() == "signal" and t.last_strategy() == "tagged"

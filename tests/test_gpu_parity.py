@@ -344,3 +344,18 @@ def test_graph_rmat_count_min(rs, strategy, mode):
     got, st, _ = run_gpu(rs, wv, offh, stages, "count_min_u32", strategy, mode, chunk=2048)
     assert_parity(got, ref, "count_min_u32")
     assert (np.diff(offh) == 0).mean() > 0.3          # R-MAT: many isolated vertices
+
+
+@pytest.mark.parametrize("L", [16, 3000])
+def test_auto_strategy(rs, L):
+    """RS_STRATEGY_AUTO: short regions run tagged, long
+    regions signal; either way the aggregates equal the oracle's."""
+    lens = synth.lengths(max(4, (1 << 17) // L), "fixed", L=L, seed=2)
+    off = synth.offsets(lens)
+    vals = synth.values(int(off[-1]), "i32", seed=3)
+    stages = synth.sweep_stages(3)
+    ref = oracle.brute(vals, off, stages, "sum_i64")
+    got, st, p = run_gpu(rs, vals, off, stages, "sum_i64", "auto")
+    assert_parity(got, ref, "sum_i64")
+    assert p.last_strategy() == ("tagged" if L < 768 else "signal")
+    assert st[0][2] == off[-1] - off[0]
