@@ -108,6 +108,8 @@ struct AggT;
 template <>
 struct AggT<20> {  // RS_OP_SUM_I64 over int32 elements
     static constexpr bool heavy = false;   // lift costs far more than a select (fused paths lift survivors only)
+    static constexpr bool group = true;    // exact inverse: segment sums as prefix differences
+    __device__ static unsigned long long sub(unsigned long long a, unsigned long long b) { return a - b; }
     using A = unsigned long long;  // two's-complement wraparound sum
     __device__ static A id() { return 0ull; }
     __device__ static A lift(uint32_t v) { return (A)(long long)(int)v; }
@@ -124,6 +126,7 @@ struct AggT<20> {  // RS_OP_SUM_I64 over int32 elements
 template <>
 struct AggT<21> {  // RS_OP_SUM_F32 over fp32 elements
     static constexpr bool heavy = false;   // lift costs far more than a select (fused paths lift survivors only)
+    static constexpr bool group = false;   // fp32: prefix differences would cancel
     using A = float;
     __device__ static A id() { return 0.0f; }
     __device__ static A lift(uint32_t v) { return __uint_as_float(v); }
@@ -140,6 +143,7 @@ struct AggT<21> {  // RS_OP_SUM_F32 over fp32 elements
 template <>
 struct AggT<22> {  // RS_OP_COUNT_MIN_U32 over uint32 elements: (count, min)
     static constexpr bool heavy = false;   // lift costs far more than a select (fused paths lift survivors only)
+    static constexpr bool group = false;   // min has no inverse
     using A = uint2;
     __device__ static A id() { return make_uint2(0u, 0xffffffffu); }
     __device__ static A lift(uint32_t v) { return make_uint2(1u, v); }
@@ -174,6 +178,8 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
 template <>
 struct AggT<23> {  // RS_OP_COUNT_XOR64 over u8 elements: (count, xor of mix64(i << 8 | byte))
     static constexpr bool heavy = true;   // lift costs far more than a select (fused paths lift survivors only)
+    static constexpr bool group = true;   // count and xor both have exact inverses
+    __device__ static ulonglong2 sub(ulonglong2 a, ulonglong2 b) { return make_ulonglong2(a.x - b.x, a.y ^ b.y); }
     using A = ulonglong2;
     __device__ static A id() { return make_ulonglong2(0ull, 0ull); }
     // item = byte | (position mod C) << 8; delta = chunk base - region start, so the

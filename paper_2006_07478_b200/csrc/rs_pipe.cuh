@@ -726,6 +726,13 @@ struct Pipe {
             return;
         }
         const uint32_t excl = cum - cnt;
+        const uint32_t maxc = __reduce_max_sync(kFull, lane < m ? cnt : 0u);
+        if (maxc <= 4) {
+            // short parts: lane i writes part i's few tags directly
+            for (uint32_t r = 0; r < maxc; ++r)
+                if (lane < m && r < cnt) T<0>()[(E<0>().qt + excl + r) & (ring0 - 1)] = key;
+            return;
+        }
         for (uint32_t base = 0; base < tot; base += 32) {
             const uint32_t rel = base + lane;
             int lo = 0;      // largest part i < m with excl_i <= rel
@@ -1069,10 +1076,22 @@ struct Pipe {
             const uint32_t le = hm & lanemask_le();
             const int seg = le ? 31 - __clz(le) : -1;     // first lane of my segment (-1: carry segment)
             A v = val;
+            if constexpr (AT::group) {
+                // exact inverse (integer sum, count, xor): one unsegmented inclusive
+                // scan, then my segment's prefix = P[lane] - P[first lane - 1]
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const A o = AT::shfl_up(v, d);
-                if (lane - d >= seg && lane >= d) v = AT::comb(o, v);
+                for (int d = 1; d < 32; d <<= 1) {
+                    const A o = AT::shfl_up(v, d);
+                    if (lane >= d) v = AT::comb(o, v);
+                }
+                const A before = AT::shfl(v, seg >= 1 ? seg - 1 : 0);
+                if (seg >= 1) v = AT::sub(v, before);
+            } else {
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const A o = AT::shfl_up(v, d);
+                    if (lane - d >= seg && lane >= d) v = AT::comb(o, v);
+                }
             }
             if (seg < 0 && act) v = AT::comb(carry, v);
             // the carry region ended exactly before this slice
