@@ -84,6 +84,10 @@ typedef enum { RS_I32 = 0, RS_U32 = 1, RS_U8 = 2, RS_F32 = 3 } rs_dtype;
 typedef enum {
     RS_STRATEGY_SIGNAL = 0,  /* Begin/End signals with credits (§3, §4.2)  */
     RS_STRATEGY_TAGGED = 1,  /* per-item region tags          */
+    RS_STRATEGY_CONTEXT = 3, /* per-lane context (§8 f2): one boundary signal {key,
+                                stamp} per region, ensembles run across boundaries, every lane
+                                computes its own region; no tags in the queues.  4-byte
+                                elements, sequential scheduler; signal_cap >= 256 (0 = 512). */
     RS_STRATEGY_AUTO = 2     /* choice made per run, transparently (§8 f1):
                                 signal when the mean region length n_elems / n_regions is at
                                 least cfg.auto_min_len, else tagged.  Both strategies give

@@ -23,7 +23,7 @@ RS_NODE_ENUMERATE, RS_NODE_FILTER, RS_NODE_TRANSFORM, RS_NODE_AGGREGATE = 1, 2, 
 OPS = {"none": 0, "hash_lt": 1, "lt_u32": 2, "class": 3, "scale_f32": 10, "affine_i32": 11,
        "sum_i64": 20, "sum_f32": 21, "count_min_u32": 22, "count_xor64": 23}
 DTYPES = {"i32": 0, "u32": 1, "u8": 2, "f32": 3}
-STRATEGIES = {"signal": 0, "tagged": 1, "auto": 2}
+STRATEGIES = {"signal": 0, "tagged": 1, "auto": 2, "context": 3}
 STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
 RS_FLAG_STATS, RS_FLAG_VALIDATE, RS_FLAG_TIMING, RS_FLAG_WARP_SPECIALIZED, RS_FLAG_PROFILE, RS_FLAG_UNFUSED = 1, 2, 4, 8, 16, 32
 

@@ -76,10 +76,10 @@ uint32_t auto_default(int nst) {
 
 bool get_launch(const rs_pipeline *p, Launch *L) {
     switch (p->agg) {
-        case RS_OP_SUM_I64: *L = launch_agg20(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
-        case RS_OP_SUM_F32: *L = launch_agg21(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
-        case RS_OP_COUNT_MIN_U32: *L = launch_agg22(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
-        case RS_OP_COUNT_XOR64: *L = launch_agg23(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage); return true;
+        case RS_OP_SUM_I64: *L = launch_agg20(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
+        case RS_OP_SUM_F32: *L = launch_agg21(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
+        case RS_OP_COUNT_MIN_U32: *L = launch_agg22(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
+        case RS_OP_COUNT_XOR64: *L = launch_agg23(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
     }
     return false;
 }
@@ -191,8 +191,11 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
         *out = p;
         return RS_OK;
     }
-    if (cfg.strategy != RS_STRATEGY_SIGNAL && cfg.strategy != RS_STRATEGY_TAGGED)
+    if (cfg.strategy != RS_STRATEGY_SIGNAL && cfg.strategy != RS_STRATEGY_TAGGED && cfg.strategy != RS_STRATEGY_CONTEXT)
         return fail(RS_ERR_INVALID_ARG, "bad strategy");
+    const bool ctx_ = cfg.strategy == RS_STRATEGY_CONTEXT;
+    if (ctx_ && (elem == RS_U8 || (cfg.flags & RS_FLAG_WARP_SPECIALIZED)))
+        return fail(RS_ERR_UNSUPPORTED, "the context strategy is built for 4-byte elements and the sequential scheduler");
     if (cfg.simd_width == 0) cfg.simd_width = W;
     if (cfg.simd_width != (uint32_t)W) return fail(RS_ERR_UNSUPPORTED, "only simd_width 128 is built");
     // Defaults tuned on B200 (profiles/r1_tuning.txt): deep queues amortise the
@@ -206,7 +209,10 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     const bool inplace = elem != RS_U8 && !(cfg.flags & RS_FLAG_WARP_SPECIALIZED);
     const bool tagged_ = cfg.strategy == RS_STRATEGY_TAGGED;
     if (cfg.queue_cap == 0) cfg.queue_cap = inplace ? (tagged_ ? 16 * W : 32 * W) : (nst_ >= 2 ? 8 * W : 16 * W);
-    if (cfg.signal_cap == 0) cfg.signal_cap = inplace ? 32 : (nst_ >= 2 ? 64 : 128);
+    if (cfg.signal_cap == 0)
+        cfg.signal_cap = cfg.strategy == RS_STRATEGY_CONTEXT ? 512 : (inplace ? 32 : (nst_ >= 2 ? 64 : 128));
+    if (cfg.strategy == RS_STRATEGY_CONTEXT && cfg.signal_cap < 2 * W)
+        return fail(RS_ERR_UNSUPPORTED, "the context strategy needs signal_cap >= 256 (one ensemble's boundaries)");
     if (cfg.q0_stage == 0)
         cfg.q0_stage = inplace ? (tagged_ ? 512 : 1024) : ((tagged_ || nst_ >= 2) ? 256 : 512);
     if (!is_pow2(cfg.queue_cap) || cfg.queue_cap < 2 * W || cfg.queue_cap > 65536)

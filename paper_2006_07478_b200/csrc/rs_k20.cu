@@ -2,7 +2,7 @@
 #include "rs_kern.cuh"
 
 namespace rsk {
-Launch launch_agg20(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk) {
-    return launch_for<20>(K, tag, fuse, qcap, scap, sblk);
+Launch launch_agg20(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx) {
+    return launch_for<20>(K, tag, fuse, qcap, scap, sblk, ctx);
 }
 }  // namespace rsk

@@ -201,20 +201,20 @@ struct Launch {
 };
 
 // One per aggregate, defined in rs_k<AGG>.cu.
-Launch launch_agg20(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk);
-Launch launch_agg21(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk);
-Launch launch_agg22(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk);
-Launch launch_agg23(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk);
+Launch launch_agg20(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
+Launch launch_agg21(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
+Launch launch_agg22(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
+Launch launch_agg23(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
 
 #ifndef RS_HOST_ONLY
-template <int AGG, bool TAG, bool FUSE>
+template <int AGG, bool TAG, bool FUSE, bool CTX = false>
 KernelFn pick_k(int K) {
     switch (K) {
-        case 0: return k_pipeline<0, AGG, TAG, false>;      // nothing to fuse
-        case 1: return k_pipeline<1, AGG, TAG, FUSE>;
-        case 2: return k_pipeline<2, AGG, TAG, FUSE>;
-        case 3: return k_pipeline<3, AGG, TAG, FUSE>;
-        default: return k_pipeline<4, AGG, TAG, FUSE>;
+        case 0: return k_pipeline<0, AGG, TAG, false, CTX>;      // nothing to fuse
+        case 1: return k_pipeline<1, AGG, TAG, FUSE, CTX>;
+        case 2: return k_pipeline<2, AGG, TAG, FUSE, CTX>;
+        case 3: return k_pipeline<3, AGG, TAG, FUSE, CTX>;
+        default: return k_pipeline<4, AGG, TAG, FUSE, CTX>;
     }
 }
 
@@ -240,32 +240,42 @@ uint32_t smem_ws(int K, uint32_t qcap, uint32_t scap) {
     }
 }
 
-template <int AGG, bool TAG, bool FUSE>
+template <int AGG, bool TAG, bool FUSE, bool CTX = false>
 uint32_t ring_for(int K, uint32_t sblk, uint32_t qcap) {
     switch (K) {
-        case 0: return Pipe<0, AGG, TAG, false>::ring_for(sblk, qcap);
-        case 1: return Pipe<1, AGG, TAG, FUSE>::ring_for(sblk, qcap);
-        case 2: return Pipe<2, AGG, TAG, FUSE>::ring_for(sblk, qcap);
-        case 3: return Pipe<3, AGG, TAG, FUSE>::ring_for(sblk, qcap);
-        default: return Pipe<4, AGG, TAG, FUSE>::ring_for(sblk, qcap);
+        case 0: return Pipe<0, AGG, TAG, false, CTX>::ring_for(sblk, qcap);
+        case 1: return Pipe<1, AGG, TAG, FUSE, CTX>::ring_for(sblk, qcap);
+        case 2: return Pipe<2, AGG, TAG, FUSE, CTX>::ring_for(sblk, qcap);
+        case 3: return Pipe<3, AGG, TAG, FUSE, CTX>::ring_for(sblk, qcap);
+        default: return Pipe<4, AGG, TAG, FUSE, CTX>::ring_for(sblk, qcap);
     }
 }
 
-template <int AGG, bool TAG, bool FUSE>
+template <int AGG, bool TAG, bool FUSE, bool CTX = false>
 uint32_t smem_for(int K, uint32_t qcap, uint32_t scap, uint32_t ring) {
     switch (K) {
-        case 0: return Pipe<0, AGG, TAG, false>::smem_bytes(qcap, scap, ring);
-        case 1: return Pipe<1, AGG, TAG, FUSE>::smem_bytes(qcap, scap, ring);
-        case 2: return Pipe<2, AGG, TAG, FUSE>::smem_bytes(qcap, scap, ring);
-        case 3: return Pipe<3, AGG, TAG, FUSE>::smem_bytes(qcap, scap, ring);
-        default: return Pipe<4, AGG, TAG, FUSE>::smem_bytes(qcap, scap, ring);
+        case 0: return Pipe<0, AGG, TAG, false, CTX>::smem_bytes(qcap, scap, ring);
+        case 1: return Pipe<1, AGG, TAG, FUSE, CTX>::smem_bytes(qcap, scap, ring);
+        case 2: return Pipe<2, AGG, TAG, FUSE, CTX>::smem_bytes(qcap, scap, ring);
+        case 3: return Pipe<3, AGG, TAG, FUSE, CTX>::smem_bytes(qcap, scap, ring);
+        default: return Pipe<4, AGG, TAG, FUSE, CTX>::smem_bytes(qcap, scap, ring);
     }
 }
 
 
 template <int AGG>
-Launch launch_for(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk) {
+Launch launch_for(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx = false) {
     Launch L;
+    if constexpr (AGG != 23) {      // per-lane context strategy: 4-byte (in-place) element streams
+        if (ctx) {
+            L = launch_for<AGG>(K, false, fuse, qcap, scap, sblk, false);
+            L.main = fuse ? pick_k<AGG, false, true, true>(K) : pick_k<AGG, false, false, true>(K);
+            L.ring0 = fuse ? ring_for<AGG, false, true, true>(K, sblk, qcap) : ring_for<AGG, false, false, true>(K, sblk, qcap);
+            L.inst_bytes = fuse ? smem_for<AGG, false, true, true>(K, qcap, scap, L.ring0)
+                                : smem_for<AGG, false, false, true>(K, qcap, scap, L.ring0);
+            return L;
+        }
+    }
     L.main = tag ? (fuse ? pick_k<AGG, true, true>(K) : pick_k<AGG, true, false>(K))
                  : (fuse ? pick_k<AGG, false, true>(K) : pick_k<AGG, false, false>(K));
     L.ws = tag ? pick_ws<AGG, true>(K) : pick_ws<AGG, false>(K);

@@ -296,7 +296,15 @@ struct Chunk {
 // inside one region, so the result is the same as with a separate node (the
 // tagged strategy folds by key as before).  FUSE=false is the paper's node
 // structure, kept for RS_FLAG_UNFUSED.
-template <int K, int AGG, bool TAG, bool FUSE>
+// CTX: the per-lane context strategy: no
+// tags in the queues and no boundary-limited ensembles.  Each signal is one
+// region boundary {key, stamp}: the count of items its edge carried before the
+// region's first item.  Ensembles run across boundaries; a FILTER/TRANSFORM
+// node re-stamps every boundary inside an ensemble from the ensemble's ballots
+// (survivors before it), and the aggregate gives each lane the key of the last
+// boundary at or before its item -- the context computed per lane instead of
+// stored with the items.
+template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false>
 struct Pipe {
     using AT = AggT<AGG>;
     using A = typename AT::A;
@@ -319,8 +327,8 @@ struct Pipe {
     // per-instance shared header: [0,64) TMA barriers, [64,160) node counters
     // (u32 x 24: data firings, full firings, items, signals per node),
     // [160,288) RS_FLAG_PROFILE cycle counters (u64 x 16)
-    static constexpr uint32_t HDR = 288;
-    static constexpr uint32_t CNT_OFF = 64, PROF_OFF = 160;
+    static constexpr uint32_t HDR = CTX ? 416 : 288;     // CTX: + 32-word key scratch at [288, 416)
+    static constexpr uint32_t CNT_OFF = 64, PROF_OFF = 160, SCR_OFF = 288;
 
     const KParams &P;
     const int lane;
@@ -586,6 +594,13 @@ struct Pipe {
         E<e>().sent = 0;
     }
 
+    // CTX: append boundary {key, stamp} to edge e's signal queue.
+    template <int e>
+    __device__ __forceinline__ void push_ctx(uint32_t key, uint32_t stamp) {
+        if (lane == 0) S<e>()[E<e>().st & smask] = make_uint2(key, stamp);
+        E<e>().st += 1;
+    }
+
     // One enumerate firing (resumable mid-region):
     // emit F0's parts -- Begin, element indices (as staged element values),
     // End -- as far as staged data and signal space allow.  Up to 32 parts are
@@ -635,7 +650,7 @@ struct Pipe {
             if (lane == 0 && ps < e_next) ps = e_next;     // resume inside part pidx
             const uint32_t cnt = (uint32_t)(pe - ps);
             uint32_t cum = cnt;
-            const uint32_t sig = TAG ? 0u : ((lane == 0 && begun) ? 1u : 2u);
+            const uint32_t sig = TAG ? 0u : ((lane == 0 && begun) ? (CTX ? 0u : 1u) : (CTX ? 1u : 2u));
             uint32_t scum = sig;
 #pragma unroll
             for (int dd = 1; dd < 32; dd <<= 1) {
@@ -648,7 +663,13 @@ struct Pipe {
             const uint32_t m = __popc(__ballot_sync(kFull, fits));
             if (m > 0) {
                 const uint32_t tot = __shfl_sync(kFull, cum, m - 1);
-                if constexpr (!TAG) {
+                if constexpr (CTX) {
+                    // one boundary per part not yet begun, stamped with the edge-0
+                    // count of the part's first item
+                    const uint32_t base_cnt = E<0>().qt - q_start[0];
+                    if (lane < (int)m && sig) S<0>()[(E<0>().st + scum - sig) & smask] = make_uint2(key, base_cnt + cum - cnt);
+                    E<0>().st += __shfl_sync(kFull, scum, m - 1);
+                } else if constexpr (!TAG) {
                     // Begin_i, End_i of parts 0..m-1 in stream order.
                     const bool empty_at_start = (E<0>().sh == E<0>().st);
                     const uint32_t qlen0 = E<0>().qt - E<0>().qh;
@@ -689,7 +710,8 @@ struct Pipe {
             if constexpr (!TAG) {
                 if (!begun) {
                     if (scap - (E<0>().st - E<0>().sh) == 0) return prog;
-                    push_signal<0>(key0, false, E<0>().sent);
+                    if constexpr (CTX) push_ctx<0>(key0, E<0>().qt - q_start[0]);
+                    else push_signal<0>(key0, false, E<0>().sent);
                     begun = true;
                     did = true;
                 }
@@ -701,7 +723,9 @@ struct Pipe {
                 E<0>().sent += k;
                 did = true;
             }
-            if constexpr (!TAG) {
+            if constexpr (CTX) {
+                if (k == cnt0) { pidx++; begun = false; did = true; }
+            } else if constexpr (!TAG) {
                 if (k == cnt0 && scap - (E<0>().st - E<0>().sh) > 0) {
                     push_signal<0>(key0, true, E<0>().sent);
                     pidx++;
@@ -1002,6 +1026,281 @@ struct Pipe {
         return prog;
     }
 
+    // ----------------------------------------------- per-lane context (CTX)
+    // Close the open region (akey: uniform partial `carry` + per-lane `acc`)
+    // and open `key` (a::end then a::begin).
+    __device__ __forceinline__ void ctx_close(uint32_t key) {
+        if (akey != 0xffffffffu) {
+            const A v = AT::comb(carry, warp_reduce<AT>(acc));
+            if (lane == 0) store_key(akey, v);
+        }
+        acc = AT::id();
+        carry = AT::id();
+        akey = key;
+    }
+
+    // Fire node n under CTX: full ensembles run across boundaries; a
+    // boundary at the consumption point is forwarded (re-stamped) or, at the
+    // aggregate, closes/opens a region; partial ensembles only at the drained
+    // tail (full-first, A8).
+    template <int n>
+    __device__ __forceinline__ bool fire_ctx(bool drained) {
+        constexpr int ei = n - 1;
+        constexpr bool AGGN = (n == K + 1) || (NA && n == K);
+        const uint32_t imask = qm<ei>();
+        const uint32_t *in = Q<ei>();
+        bool prog = false;
+        uint32_t ready_lim = 0;
+        if (ei == 0) ready_lim = landed_pos();
+        for (;;) {
+            const uint32_t a = E<ei>().qt - E<ei>().qh;
+            uint32_t ar = a;
+            if (ei == 0) {
+                if ((int)(ready_lim - E<0>().qh) < (int)ar) ready_lim = landed_pos();
+                const int rdy = (int)(ready_lim - E<0>().qh);
+                ar = rdy <= 0 ? 0u : min(ar, (uint32_t)rdy);
+            }
+            const uint32_t cons = E<ei>().qh - q_start[ei];
+            const bool sp = E<ei>().sh != E<ei>().st;
+            uint2 hs = make_uint2(0u, 0u);
+            if (sp) hs = S<ei>()[E<ei>().sh & smask];
+            const uint32_t srel = sp ? hs.y - cons : 0xffffffffu;
+            if (sp && srel == 0) {
+                if constexpr (AGGN) {
+                    ctx_close(hs.x);
+                } else {
+                    if (scap - (E<n>().st - E<n>().sh) == 0) break;
+                    push_ctx<n>(hs.x, E<n>().qt - q_start[n]);
+                }
+                E<ei>().sh++;
+                prog = true;
+                continue;
+            }
+            uint32_t nclean = ar / W;
+            if (sp) nclean = min(nclean, srel / W);
+            if (nclean > 0) {
+                run_full<n>(in, nullptr, imask, E<ei>().qh, nclean);
+                E<ei>().qh += nclean * W;
+                prog = true;
+                continue;
+            }
+            const uint32_t e = min(ar, (uint32_t)W);
+            if (e == 0) break;
+            // a partial ensemble fires when the upstream is drained, or when the
+            // input boundary queue is half full (runs of empty regions could
+            // otherwise fill it while fewer than w items wait -- reading R3)
+            if (e < (uint32_t)W && !(drained && e == a) && 2 * (E<ei>().st - E<ei>().sh) < scap) break;
+            uint32_t done = e;
+            if constexpr (AGGN) {
+                if constexpr (n == K + 1) ctx_agg_ens(in, imask, E<ei>().qh, e, cons, OpAll{});
+                else with_op(P.st[n - 1], [&](auto op) { ctx_agg_ens(in, imask, E<ei>().qh, e, cons, op); });
+            } else {
+                with_op(P.st[n - 1], [&](auto op) { done = ctx_filter_ens<n>(in, imask, E<ei>().qh, e, cons, op); });
+            }
+            if (done == 0) break;
+            E<ei>().qh += done;
+            if (done < (uint32_t)W) {
+                stat_add(n, 0, 1u);
+                stat_add(n, 1, done);
+            }
+            prog = true;
+        }
+        __syncwarp();
+        return prog;
+    }
+
+    // CTX filter: one ensemble of e items at h (consumed count cons) with
+    // boundaries strictly inside; the survivors are compacted as usual and each
+    // inside boundary is forwarded with stamp = survivors before it.  When the
+    // output signal queue cannot take all of them (runs of empty regions), the
+    // ensemble is cut before the first boundary that does not fit.  Returns
+    // the items consumed (0: the output signal queue is full).
+    template <int n, class Op>
+    __device__ __forceinline__ uint32_t ctx_filter_ens(const uint32_t *in, uint32_t imask, uint32_t h, uint32_t e,
+                                                       uint32_t cons, const Op op) {
+        constexpr int ei = n - 1;
+        const uint32_t freeo = scap - (E<n>().st - E<n>().sh);
+        // boundaries with cons < stamp < cons + e (stamps are non-decreasing)
+        uint32_t nb = 0;
+        for (;;) {
+            const uint32_t i = E<ei>().sh + nb + lane;
+            bool in_ens = false;
+            if (i - E<ei>().sh < E<ei>().st - E<ei>().sh) in_ens = S<ei>()[i & smask].y - cons < e;
+            const uint32_t b = __ballot_sync(kFull, in_ens);
+            const uint32_t c = __popc(~b) ? (uint32_t)(__ffs(~b) - 1) : 32u;   // leading run of in-ensemble entries
+            nb += c;
+            if (c < 32 || nb > freeo) break;
+        }
+        if (nb > freeo) {
+            if (freeo == 0) return 0u;
+            e = S<ei>()[(E<ei>().sh + freeo) & smask].y - cons;     // cut before boundary #freeo
+            nb = 0;                                                  // boundaries with rel < e (<= freeo)
+            for (;;) {
+                const uint32_t i = nb + lane;
+                const bool in_ens = i < freeo && S<ei>()[(E<ei>().sh + i) & smask].y - cons < e;
+                const uint32_t b = __ballot_sync(kFull, in_ens);
+                const uint32_t c = __popc(~b) ? (uint32_t)(__ffs(~b) - 1) : 32u;
+                nb += c;
+                if (c < 32) break;
+            }
+        }
+        const uint32_t qm_ = qm<n>();
+        uint32_t *out = Q<n>();
+        uint32_t tl = E<n>().qt;
+        const uint32_t t0 = tl - q_start[n];
+        uint32_t mk[IPL];
+#pragma unroll
+        for (int j = 0; j < IPL; ++j) {
+            const uint32_t idx = j * 32 + lane;
+            const bool act = idx < e;
+            uint32_t v = act ? in[(h + idx) & imask] : 0u;
+            const bool keep = act && op(v);
+            mk[j] = __ballot_sync(kFull, keep);
+            if (keep) out[(tl + __popc(mk[j] & lt)) & qm_] = v;
+            tl += __popc(mk[j]);
+        }
+        // re-stamp the inside boundaries, 32 at a time
+        for (uint32_t b0 = 0; b0 < nb; b0 += 32) {
+            if (b0 + lane < nb) {
+                const uint2 sg = S<ei>()[(E<ei>().sh + b0 + lane) & smask];
+                const uint32_t rel = sg.y - cons;                  // 1 .. e-1
+                const uint32_t j = rel >> 5, l = rel & 31u;
+                uint32_t before = 0;
+#pragma unroll
+                for (int jj = 0; jj < IPL; ++jj) {
+                    if ((uint32_t)jj < j) before += __popc(mk[jj]);
+                    else if ((uint32_t)jj == j) before += __popc(mk[jj] & ((1u << l) - 1u));
+                }
+                S<n>()[(E<n>().st + b0 + lane) & smask] = make_uint2(sg.x, t0 + before);
+            }
+        }
+        __syncwarp();
+        E<ei>().sh += nb;
+        E<n>().st += nb;
+        E<n>().qt = tl;
+        return e;
+    }
+
+    // CTX aggregate: one ensemble of e items at h (consumed count cons); each
+    // 32-item slice folds its items into the region of the last boundary at or
+    // before them (segmented like the tagged fold, keys computed per lane).
+    template <class Op>
+    __device__ __forceinline__ void ctx_agg_ens(const uint32_t *in, uint32_t imask, uint32_t h, uint32_t e,
+                                                uint32_t cons, const Op op) {
+        constexpr int ei = NA ? K - 1 : K;
+        uint32_t *scr = reinterpret_cast<uint32_t *>(base + SCR_OFF);
+#pragma unroll 1
+        for (uint32_t j = 0; j * 32 < e; ++j) {
+            const uint32_t p0 = cons + 32 * j;                     // consumed count at the slice start
+            const uint32_t cntj = min(e - 32 * j, 32u);
+            // boundaries exactly at the slice start: close/open in order (empty regions included)
+            for (;;) {
+                if (E<ei>().sh == E<ei>().st) break;
+                const uint2 hs = S<ei>()[E<ei>().sh & smask];
+                if (hs.y != p0) break;
+                ctx_close(hs.x);
+                E<ei>().sh++;
+            }
+            const bool act = lane < cntj;
+            uint32_t x = act ? in[(h + 32 * j + lane) & imask] : 0u;
+            const bool keep = act && op(x);
+            if constexpr (NA) fkept += keep ? 1u : 0u;
+            const A val = keep ? AT::lift_i(x, 0) : AT::id();
+            // boundaries strictly inside the slice (rel 1..cntj-1)
+            const uint32_t avail_s = E<ei>().st - E<ei>().sh;
+            const uint2 sg = lane < avail_s ? S<ei>()[(E<ei>().sh + lane) & smask] : make_uint2(0u, 0xffffffffu);
+            const uint32_t rel = sg.y - p0;
+            const bool inb = lane < avail_s && rel < cntj;
+            const uint32_t bm = __ballot_sync(kFull, inb);
+            if (bm == 0) {
+                acc = AT::comb(acc, val);                          // the slice continues the open region
+                continue;
+            }
+            const uint32_t nb = __popc(bm);                        // in-slice boundaries are a prefix
+            const uint32_t nrel = __shfl_down_sync(kFull, rel, 1);
+            const bool dup = inb && lane + 1 < nb && nrel == rel;  // an empty region (same stamp as the next)
+            if (__any_sync(kFull, dup) || nb == 32) {
+                // rare: empty regions inside the slice or a full slice of boundaries --
+                // fold item by item in stream order between the boundaries
+                ctx_agg_slice_serial(val, cntj, p0);
+                continue;
+            }
+            if (inb) scr[rel] = sg.x;
+            __syncwarp();
+            const uint32_t hm = __reduce_or_sync(kFull, inb ? (1u << rel) : 0u);
+            const uint32_t le = hm & lanemask_le();
+            const int seg = le ? 31 - __clz(le) : -1;             // first lane of my segment (-1: open region)
+            const uint32_t key = seg >= 0 ? scr[seg] : akey;
+            __syncwarp();
+            // fold the per-lane partials of the open region into `carry`
+            carry = AT::comb(carry, warp_reduce<AT>(acc));
+            acc = AT::id();
+            A v = val;
+            if constexpr (AT::group) {
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const A o = AT::shfl_up(v, d);
+                    if (lane >= d) v = AT::comb(o, v);
+                }
+                const A before = AT::shfl(v, seg >= 1 ? seg - 1 : 0);
+                if (seg >= 1) v = AT::sub(v, before);
+            } else {
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const A o = AT::shfl_up(v, d);
+                    if (lane - d >= seg && lane >= d) v = AT::comb(o, v);
+                }
+            }
+            if (seg < 0) v = AT::comb(carry, v);
+            const bool nexthead = (lane < 31) && ((hm >> (lane + 1)) & 1u);
+            if (act && nexthead) {                                 // a segment ends inside the slice
+                if (key != 0xffffffffu) store_key(key, v);
+            }
+            const int last = (int)cntj - 1;
+            akey = __shfl_sync(kFull, key, last);
+            carry = AT::shfl(v, last);
+            E<ei>().sh += nb;
+        }
+    }
+
+    // Slow path of ctx_agg_ens: every boundary inside the slice (any number,
+    // empty regions included), one at a time in stream order.
+    __device__ __noinline__ void ctx_agg_slice_serial(A val, uint32_t cntj, uint32_t p0) {
+        constexpr int ei = NA ? K - 1 : K;
+        uint32_t from = 0;
+        while (E<ei>().sh != E<ei>().st) {
+            const uint2 hs = S<ei>()[E<ei>().sh & smask];
+            const uint32_t rel = hs.y - p0;
+            if (rel >= cntj) break;
+            if (lane >= from && lane < rel) acc = AT::comb(acc, val);
+            ctx_close(hs.x);
+            E<ei>().sh++;
+            from = rel;
+        }
+        if (lane >= from && lane < cntj) acc = AT::comb(acc, val);
+    }
+
+    // Scheduler state of a stuck instance (workspace bytes [64, 256), read by
+    // tools/dbg_ctx.py): per edge qh, qt, sh, st, q_start, head signal word.
+    template <int e = 0>
+    __device__ __forceinline__ void dump_edges(uint32_t *d) {
+        if constexpr (e <= K && e < 4) {
+            d[8 + 6 * e + 0] = E<e>().qh; d[8 + 6 * e + 1] = E<e>().qt;
+            d[8 + 6 * e + 2] = E<e>().sh; d[8 + 6 * e + 3] = E<e>().st;
+            d[8 + 6 * e + 4] = q_start[e];
+            d[8 + 6 * e + 5] = (E<e>().sh != E<e>().st) ? S<e>()[E<e>().sh & smask].y : 0xdeadu;
+            dump_edges<e + 1>(d);
+        }
+    }
+    __device__ __noinline__ void watchdog_dump(uint32_t why) {
+        if constexpr (!U8) {   // (nvcc 12.9 cicc crashes on this body in the u8 instantiation with -lineinfo)
+            uint32_t *d = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(P.hdr) + 64);
+            d[0] = 0xd0d0u | (why << 16); d[1] = enum_done; d[2] = claims_done; d[3] = (uint32_t)F0.k; d[4] = stg_j;
+            d[5] = landed_j; d[6] = blockIdx.x * 32 + (threadIdx.x >> 5); d[7] = scap;
+            dump_edges<0>(d);
+        }
+    }
+
     __device__ __forceinline__ void store_key(uint32_t key, A v) {
         if (key & SLOT) AT::store(P.part0, P.part1, key & ~SLOT, v);
         else AT::store(P.out0, P.out1, key, v);
@@ -1147,7 +1446,9 @@ struct Pipe {
             return false;
         } else {
             const long long t0 = prof ? clock64() : 0;
-            const bool p = fire<n>(drained);
+            bool p;
+            if constexpr (CTX) p = fire_ctx<n>(drained);
+            else p = fire<n>(drained);
             if (prof) pcnt(n, clock64() - t0);
             const bool dn = drained && (E<n - 1>().qh == E<n - 1>().qt) && (E<n - 1>().sh == E<n - 1>().st);
             return fire_chain<n + 1>(dn) | p;
@@ -1218,18 +1519,19 @@ struct Pipe {
                     if (++spins > (1u << 24)) break;
                 }
                 if (spins > (1u << 24)) {
-                    if (lane == 0) atomicCAS((int *)&P.hdr->err, 0, ERR_WATCHDOG);
+                    if (lane == 0 && atomicCAS((int *)&P.hdr->err, 0, ERR_WATCHDOG) == 0) watchdog_dump(1u);
                     break;
                 }
                 if (prof) { pcnt(K + 2, clock64() - tw); pcnt(9, 1); }
                 continue;
             }
             if (++idle > 64) {
-                if (lane == 0) atomicCAS((int *)&P.hdr->err, 0, ERR_WATCHDOG);
+                if (lane == 0 && atomicCAS((int *)&P.hdr->err, 0, ERR_WATCHDOG) == 0) watchdog_dump(2u);
                 break;
             }
         }
         if constexpr (TAG) flush_tagged();
+        if constexpr (CTX) ctx_close(0xffffffffu);
         // drain outstanding TMA stages before the CTA's shared memory is released
         for (uint32_t spins = 0; landed_j < stg_j && spins < (1u << 26); ++spins) {
             if (mbar_try_wait_uniform(&bar[landed_j & (nstg - 1)], (landed_j >> nsh) & 1u)) landed_j++;
@@ -1246,12 +1548,12 @@ struct Pipe {
     }
 };
 
-template <int K, int AGG, bool TAG, bool FUSE>
+template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false>
 __global__ void __launch_bounds__(WPB_MAX * 32, 1) k_pipeline(const __grid_constant__ KParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    using PP = Pipe<K, AGG, TAG, FUSE>;
+    using PP = Pipe<K, AGG, TAG, FUSE, CTX>;
     uint8_t *mine = smem + (size_t)warp * PP::smem_bytes(P.qcap, P.scap, P.ring0);
     if (P.hdr->err) return;
     PP pipe(P, mine, lane);

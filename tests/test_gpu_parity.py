@@ -114,26 +114,32 @@ def _case(seed, agg, R=None, dist=None, L=None, base=None):
 
 
 @pytest.mark.parametrize("seed", range(24))
-@pytest.mark.parametrize("strategy", ["signal", "tagged"])
+@pytest.mark.parametrize("strategy", ["signal", "tagged", "context"])
 @pytest.mark.parametrize("mode", ["ws", "seq", "unfused"])
 def test_random_parity(rs, seed, strategy, mode):
+    if strategy == "context" and mode == "ws":
+        pytest.skip("the context strategy is built for the sequential scheduler")
     agg = ["sum_i64", "sum_f32", "count_min_u32"][seed % 3]
     vals, off, stages = _case(seed, agg)
     rnd = random.Random(seed * 7 + 1)
     cfg = dict(chunk=rnd.choice([2048, 4096, 8192]), grid=rnd.choice([0, 0, 1, 3]),
                queue_cap=rnd.choice([256, 512]), signal_cap=rnd.choice([4, 16, 128]),
                q0_stage=rnd.choice([0, 128, 256]))   # in-place rings down to 512 items (heavy relocation)
+    if strategy == "context":
+        cfg["signal_cap"] = rnd.choice([256, 512])
     ref = oracle.brute(vals, off, stages, agg)
     got, st, _ = run_gpu(rs, vals, off, stages, agg, strategy, mode, **cfg)
     assert_parity(got, ref, agg)
     assert st[0][2] == off[-1] - off[0]
 
 
-@pytest.mark.parametrize("strategy", ["signal", "tagged"])
+@pytest.mark.parametrize("strategy", ["signal", "tagged", "context"])
 @pytest.mark.parametrize("L", [1, 4, 32, 127, 128, 129, 256, 4096, 100000])
 @pytest.mark.parametrize("mode", ["ws", "seq", "unfused"])
 def test_region_lengths(rs, strategy, L, mode):
     """Region lengths 1..4096 (north star) plus regions far longer than a chunk."""
+    if strategy == "context" and mode == "ws":
+        pytest.skip("the context strategy is built for the sequential scheduler")
     N = 1 << 18
     R = max(1, N // L)
     for dist in ("fixed", "var"):
@@ -146,7 +152,7 @@ def test_region_lengths(rs, strategy, L, mode):
         assert_parity(got, ref, "sum_i64")
 
 
-@pytest.mark.parametrize("strategy", ["signal", "tagged"])
+@pytest.mark.parametrize("strategy", ["signal", "tagged", "context"])
 def test_empty_and_degenerate(rs, strategy):
     stages = synth.sweep_stages(2)
     # all regions empty (N = 0)
@@ -175,7 +181,9 @@ def test_strategies_bit_identical(rs):
     stages = synth.sweep_stages(3)
     a, _, _ = run_gpu(rs, vals, off, stages, "sum_i64", "signal")
     b, _, _ = run_gpu(rs, vals, off, stages, "sum_i64", "tagged")
+    c, _, _ = run_gpu(rs, vals, off, stages, "sum_i64", "context")
     np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[0], c[0])
 
 
 def test_batching_invariance(rs):
@@ -359,3 +367,26 @@ def test_auto_strategy(rs, L):
     assert_parity(got, ref, "sum_i64")
     assert p.last_strategy() == ("tagged" if L < 768 else "signal")
     assert st[0][2] == off[-1] - off[0]
+
+
+@pytest.mark.parametrize("thr", [0, 1, 64, 256])
+@pytest.mark.parametrize("L", [1, 3, 40, 300])
+def test_context_empty_region_runs(rs, thr, L):
+    """Per-lane context strategy under runs of empty regions:
+    heavy filters leave most regions without survivors, so many boundaries share
+    a stamp and fill the boundary queues (reading R3 cuts ensembles / fires
+    partials under that pressure); aggregates, counts and per-node items exact."""
+    lens = synth.lengths(max(8, (1 << 16) // L), "var", L=L, seed=L + thr)
+    off = synth.offsets(lens, base=1)
+    vals = synth.values(int(off[-1]) + 3, "i32", seed=thr + 1)
+    stages = [("hash_lt", 0x9E3779B1, thr), ("hash_lt", 0x85EBCA6B, 192)]
+    for agg in ("sum_i64", "sum_f32", "count_min_u32"):
+        v = synth.values(int(off[-1]) + 3, AGG_DTYPE[agg], seed=thr + 2) if agg != "sum_i64" else vals
+        st = stages if agg != "count_min_u32" else [("lt_u32", thr << 24), ("lt_u32", 3 << 30)]
+        ref = oracle.brute(v, off, st, agg)
+        for mode in ("seq", "unfused"):
+            got, stt, _ = run_gpu(rs, v, off, st, agg, "context", mode, grid=1, signal_cap=256)
+            assert_parity(got, ref, agg)
+            kc = oracle.node_counts(v, off, st)
+            for j in range(len(st) + 1):
+                assert stt[j + 1][2] == kc[:, j].sum()
