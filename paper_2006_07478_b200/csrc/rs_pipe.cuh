@@ -1217,17 +1217,20 @@ struct Pipe {
                 continue;
             }
             const uint32_t nb = __popc(bm);                        // in-slice boundaries are a prefix
-            const uint32_t nrel = __shfl_down_sync(kFull, rel, 1);
-            const bool dup = inb && lane + 1 < nb && nrel == rel;  // an empty region (same stamp as the next)
-            if (__any_sync(kFull, dup) || nb == 32) {
-                // rare: empty regions inside the slice or a full slice of boundaries --
-                // fold item by item in stream order between the boundaries
+            if (nb == 32) {
+                // 32 or more boundaries in 32 items: one at a time in stream order
                 ctx_agg_slice_serial(val, cntj, p0);
                 continue;
             }
-            if (inb) scr[rel] = sg.x;
+            const uint32_t nrel = __shfl_down_sync(kFull, rel, 1);
+            // an empty region (same stamp as the next boundary): identity now (A1);
+            // the last boundary of each stamp starts the segment
+            const bool dup = inb && lane + 1 < nb && nrel == rel;
+            if (dup) store_key(sg.x, AT::id());
+            const bool eff = inb && !dup;
+            if (eff) scr[rel] = sg.x;
             __syncwarp();
-            const uint32_t hm = __reduce_or_sync(kFull, inb ? (1u << rel) : 0u);
+            const uint32_t hm = __reduce_or_sync(kFull, eff ? (1u << rel) : 0u);
             const uint32_t le = hm & lanemask_le();
             const int seg = le ? 31 - __clz(le) : -1;             // first lane of my segment (-1: open region)
             const uint32_t key = seg >= 0 ? scr[seg] : akey;
@@ -1265,7 +1268,7 @@ struct Pipe {
 
     // Slow path of ctx_agg_ens: every boundary inside the slice (any number,
     // empty regions included), one at a time in stream order.
-    __device__ __noinline__ void ctx_agg_slice_serial(A val, uint32_t cntj, uint32_t p0) {
+    __device__ __forceinline__ void ctx_agg_slice_serial(A val, uint32_t cntj, uint32_t p0) {
         constexpr int ei = NA ? K - 1 : K;
         uint32_t from = 0;
         while (E<ei>().sh != E<ei>().st) {
@@ -1292,7 +1295,7 @@ struct Pipe {
             dump_edges<e + 1>(d);
         }
     }
-    __device__ __noinline__ void watchdog_dump(uint32_t why) {
+    __device__ __forceinline__ void watchdog_dump(uint32_t why) {   // (a noinline member would force the whole instance state into local memory)
         if constexpr (!U8) {   // (nvcc 12.9 cicc crashes on this body in the u8 instantiation with -lineinfo)
             uint32_t *d = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(P.hdr) + 64);
             d[0] = 0xd0d0u | (why << 16); d[1] = enum_done; d[2] = claims_done; d[3] = (uint32_t)F0.k; d[4] = stg_j;

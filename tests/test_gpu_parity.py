@@ -126,7 +126,7 @@ def test_random_parity(rs, seed, strategy, mode):
                queue_cap=rnd.choice([256, 512]), signal_cap=rnd.choice([4, 16, 128]),
                q0_stage=rnd.choice([0, 128, 256]))   # in-place rings down to 512 items (heavy relocation)
     if strategy == "context":
-        cfg["signal_cap"] = rnd.choice([256, 512])
+        cfg["signal_cap"] = rnd.choice([4, 32, 64, 512])
     ref = oracle.brute(vals, off, stages, agg)
     got, st, _ = run_gpu(rs, vals, off, stages, agg, strategy, mode, **cfg)
     assert_parity(got, ref, agg)
@@ -384,8 +384,8 @@ def test_context_empty_region_runs(rs, thr, L):
         v = synth.values(int(off[-1]) + 3, AGG_DTYPE[agg], seed=thr + 2) if agg != "sum_i64" else vals
         st = stages if agg != "count_min_u32" else [("lt_u32", thr << 24), ("lt_u32", 3 << 30)]
         ref = oracle.brute(v, off, st, agg)
-        for mode in ("seq", "unfused"):
-            got, stt, _ = run_gpu(rs, v, off, st, agg, "context", mode, grid=1, signal_cap=256)
+        for mode, scap in (("seq", 256), ("unfused", 256), ("seq", 8), ("unfused", 32)):
+            got, stt, _ = run_gpu(rs, v, off, st, agg, "context", mode, grid=1, signal_cap=scap)
             assert_parity(got, ref, agg)
             kc = oracle.node_counts(v, off, st)
             for j in range(len(st) + 1):
