@@ -416,7 +416,7 @@ def run_configs(rs, torch, dev, args):
         spec = workload_spec(name)
         vals, off = make_inputs(spec, seed=0x5EED + 3, device=dev)
         n, R = int(off[-1].item() - off[0].item()), off.numel() - 1
-        for strat in ("signal", "tagged"):
+        for strat in ("signal", "tagged") + (("context",) if spec["dtype"] != "u8" else ()):
             p = rs.Pipeline(spec["stages"], spec["agg"], strategy=strat, flags=rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING)
             out = p.alloc_outputs(R, dev)
             ws = p.alloc_workspace(R, vals.numel(), dev)
@@ -440,7 +440,8 @@ def run_configs(rs, torch, dev, args):
 
 def run_sweep(rs, torch, dev, args):
     """Items/s and per-node lane fraction vs region length, signal vs tagged
-    (BASELINE metric; Figs. 5-6 shape).  N = 2^29 children per point."""
+    (BASELINE metric; Figs. 5-6 shape), plus the per-lane context strategy
+    (SURVEY §8 f2).  N = 2^29 children per point."""
     res = []
     Ls = [int(x) for x in args.sweep_L.split(",")]
     import synth
@@ -458,7 +459,7 @@ def run_sweep(rs, torch, dev, args):
             off = synth.torch_offsets(lens)
             n = int(off[-1].item())
             R = off.numel() - 1
-            for strat in ("signal", "tagged"):
+            for strat in ("signal", "tagged", "context"):
                 p = rs.Pipeline(synth.sweep_stages(3), "sum_i64", strategy=strat,
                                 flags=rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING)
                 out = p.alloc_outputs(R, dev)
@@ -489,7 +490,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="sweep_fixed_L4096")
-    ap.add_argument("--strategy", default="signal", choices=["signal", "tagged"])
+    ap.add_argument("--strategy", default="signal", choices=["signal", "tagged", "context", "auto"])
     ap.add_argument("--no-sweep", dest="sweep", action="store_false")
     ap.add_argument("--sweep-L", default="1,4,32,256,4096")
     ap.add_argument("--sweep-reps", type=int, default=2)
