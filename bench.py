@@ -279,9 +279,13 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # RS_DIST_BACKEND=gloo + one GPU: every rank shares cuda:0 (a functional test
+    # of the multi-rank path on a 1-GPU box; numbers from it are not scaling data)
+    backend = os.environ.get("RS_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     spec = workload_spec(args.workload)
     vals, off = make_inputs(spec, seed=0x5EED + 2 + 1000 * rank, device=dev)
@@ -325,7 +329,7 @@ def run_ours(args):
         p.run(vals, off, out, ws)
         main_ms.append(p.kernel_times()[1])
     if world > 1:
-        t = torch.tensor([total_ms], device=dev)
+        t = torch.tensor([total_ms], device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
         dist.barrier()

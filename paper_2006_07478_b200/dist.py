@@ -51,8 +51,10 @@ def gather_aggregates(local, bounds, dst: int = 0, group=None):
     sizes = [bounds[k + 1] - bounds[k] for k in range(world)]
     assert local.numel() == sizes[rank], "local shard size does not match the partition"
     m = max(sizes) if sizes else 0
-    buf = torch.zeros(m, dtype=local.dtype, device=local.device)
-    buf[: local.numel()] = local
+    # gloo moves host tensors (CPU tests, the 1-GPU functional run); NCCL device ones
+    dev = local.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    buf = torch.zeros(m, dtype=local.dtype, device=dev)
+    buf[: local.numel()] = local.to(dev)
     if rank == dst:
         parts = [torch.empty_like(buf) for _ in range(world)]
         dist.gather(buf, parts, dst=dst, group=group)
