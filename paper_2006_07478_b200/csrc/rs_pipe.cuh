@@ -491,26 +491,31 @@ struct Pipe {
         constexpr uint32_t AL = 16u / ESZ;                     // elements per 16-byte block
         const uint32_t j = stg_j;
         const uint32_t p0 = j * sblk;
-        const uint32_t n = min(sblk, c.pos + flen(c) - p0);
         const long long src = c.beg + (long long)p0 - (long long)c.pos;   // 16-byte aligned element index
         uint8_t *dst = reinterpret_cast<uint8_t *>(Q<0>()) + (size_t)(p0 & (ring0 - 1)) * ESZ;
         uint64_t *b = &bar[j & (nstg - 1)];
-        const long long lim = (P.n_elems - src) & ~(long long)(AL - 1);   // whole 16-byte blocks in the array
-        const uint32_t ntma = (uint32_t)min((long long)((n + AL - 1) & ~(AL - 1)), lim);
-        // tail elements that a 16-byte copy cannot reach without overrunning n_elems
-        const int tail = (int)n - (int)ntma;
-        if (tail > 0 && lane < tail) {
-            if constexpr (U8) dst[ntma + lane] = P.elems[src + ntma + lane];
-            else reinterpret_cast<uint32_t *>(dst)[ntma + lane] =
-                __ldg(reinterpret_cast<const uint32_t *>(P.elems) + src + ntma + lane);
+        uint32_t ntma = sblk;
+        if (p0 + sblk > c.pos + flen(c)) {
+            // the chunk's last (short) stage; a stage inside the chunk ends at or
+            // before c.end <= n_elems, so whole stages need none of this
+            const uint32_t n = c.pos + flen(c) - p0;
+            const long long lim = (P.n_elems - src) & ~(long long)(AL - 1);   // whole 16-byte blocks in the array
+            ntma = (uint32_t)min((long long)((n + AL - 1) & ~(AL - 1)), lim);
+            // tail elements that a 16-byte copy cannot reach without overrunning n_elems
+            const int tail = (int)n - (int)ntma;
+            if (tail > 0 && lane < tail) {
+                if constexpr (U8) dst[ntma + lane] = P.elems[src + ntma + lane];
+                else reinterpret_cast<uint32_t *>(dst)[ntma + lane] =
+                    __ldg(reinterpret_cast<const uint32_t *>(P.elems) + src + ntma + lane);
+            }
         }
-        // in-place rings: the slots being refilled may hold items every lane
-        // wrote through the generic proxy (compaction, relocation); order those
-        // writes before the async-proxy (TMA) writes of this stage
+        // the slots being refilled may hold items lanes wrote through the generic
+        // proxy (in-place rings: compaction, relocation; the byte tail above);
+        // order those writes before the async-proxy (TMA) writes of this stage
         if constexpr (INPLACE) fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
-            fence_proxy_async();
+            if constexpr (!INPLACE) fence_proxy_async();
             if (ntma) {
                 mbar_arrive_expect_tx(b, ntma * ESZ);
                 tma_load_1d(dst, P.elems + src * ESZ, ntma * ESZ, b);
