@@ -74,8 +74,11 @@ __device__ __forceinline__ void filter_slices(const uint32_t *in, const uint32_t
     if constexpr (TAG) {
 #pragma unroll
         for (int j = 0; j < NS; ++j) tg[j] = tin[(h + 32 * j + lane) & imask];
-        __syncwarp();   // in-place rings: tag reads of all lanes precede the tag stores below
     }
+    // in-place rings: every lane's reads of this ensemble are ordered before any
+    // lane's compaction stores into the same slots (the memory ordering of
+    // __syncwarp; ballots order execution, not memory)
+    __syncwarp();
 #pragma unroll
     for (int j = 0; j < NS; ++j) keep[j] = op(v[j]);
     uint32_t mk[NS];
@@ -110,23 +113,24 @@ __device__ __noinline__ uint32_t partial_stage(const Op op, const uint32_t *in, 
                                                uint32_t imask, uint32_t h, uint32_t e, uint32_t *out, uint32_t *tout,
                                                uint32_t qmask, uint32_t tl, uint32_t lt, uint32_t cmask) {
     const uint32_t lane = threadIdx.x & 31u;
+    uint32_t v[IPL], tg[IPL];
+#pragma unroll
+    for (int j = 0; j < IPL; ++j) {
+        const uint32_t idx = j * 32 + lane;
+        const bool act = idx < e;
+        v[j] = act ? load_item<U8IN>(in, h + idx, imask, cmask) : 0u;
+        if constexpr (TAG) tg[j] = act ? tin[(h + idx) & imask] : 0u;
+    }
+    __syncwarp();   // in-place rings: all reads before any compaction store
 #pragma unroll
     for (int j = 0; j < IPL; ++j) {
         if ((uint32_t)j * 32u >= e) break;
-        const uint32_t idx = j * 32 + lane;
-        const bool act = idx < e;
-        uint32_t v = act ? load_item<U8IN>(in, h + idx, imask, cmask) : 0u;
-        uint32_t tg = 0;
-        if constexpr (TAG) {
-            tg = act ? tin[(h + idx) & imask] : 0u;
-            __syncwarp();   // in-place rings: tag reads precede the tag stores
-        }
-        const bool keep = act && op(v);
+        const bool keep = (j * 32 + lane) < e && op(v[j]);
         const uint32_t mk = __ballot_sync(kFull, keep);   // stable compaction
         if (keep) {
             const uint32_t pos = (tl + __popc(mk & lt)) & qmask;
-            out[pos] = v;
-            if constexpr (TAG) tout[pos] = tg;
+            out[pos] = v[j];
+            if constexpr (TAG) tout[pos] = tg[j];
         }
         tl += __popc(mk);
     }
@@ -1153,15 +1157,15 @@ struct Pipe {
         uint32_t *out = Q<n>();
         uint32_t tl = E<n>().qt;
         const uint32_t t0 = tl - q_start[n];
-        uint32_t mk[IPL];
+        uint32_t mk[IPL], v[IPL];
+#pragma unroll
+        for (int j = 0; j < IPL; ++j) v[j] = (j * 32 + lane) < e ? in[(h + j * 32 + lane) & imask] : 0u;
+        __syncwarp();   // in-place rings: all reads before any compaction store
 #pragma unroll
         for (int j = 0; j < IPL; ++j) {
-            const uint32_t idx = j * 32 + lane;
-            const bool act = idx < e;
-            uint32_t v = act ? in[(h + idx) & imask] : 0u;
-            const bool keep = act && op(v);
+            const bool keep = (j * 32 + lane) < e && op(v[j]);
             mk[j] = __ballot_sync(kFull, keep);
-            if (keep) out[(tl + __popc(mk[j] & lt)) & qm_] = v;
+            if (keep) out[(tl + __popc(mk[j] & lt)) & qm_] = v[j];
             tl += __popc(mk[j]);
         }
         // re-stamp the inside boundaries, 32 at a time
