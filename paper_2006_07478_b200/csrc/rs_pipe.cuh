@@ -84,15 +84,30 @@ __device__ __forceinline__ void filter_slices(const uint32_t *in, const uint32_t
     uint32_t mk[NS];
 #pragma unroll
     for (int j = 0; j < NS; ++j) mk[j] = __ballot_sync(kFull, keep[j]);
+    // slice bases from a shallow sum tree (not a serial chain through tl)
+    uint32_t c[NS], bs[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) c[j] = __popc(mk[j]);
+    bs[0] = tl;
+#pragma unroll
+    for (int j = 1; j < NS; ++j) {
+        uint32_t pre = 0;
+#pragma unroll
+        for (int i = 0; i < j; ++i) pre += c[i];
+        bs[j] = tl + pre;
+    }
 #pragma unroll
     for (int j = 0; j < NS; ++j) {
         if (keep[j]) {
-            const uint32_t pos = (tl + __popc(mk[j] & lt)) & qmask;
+            const uint32_t pos = (bs[j] + __popc(mk[j] & lt)) & qmask;
             out[pos] = v[j];
             if constexpr (TAG) tout[pos] = tg[j];
         }
-        tl += __popc(mk[j]);
     }
+    uint32_t all = 0;
+#pragma unroll
+    for (int j = 0; j < NS; ++j) all += c[j];
+    tl += all;
 }
 
 template <bool TAG, class Op, bool U8IN = false>
