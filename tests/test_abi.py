@@ -130,3 +130,18 @@ def test_auto_strategy_host_side(rs):
     for R, N in ((10, 1000), (1 << 20, 1 << 24)):
         assert p.workspace_bytes(R, N) == max(s.workspace_bytes(R, N), t.workspace_bytes(R, N))
     assert s.last_strategy() == "signal" and t.last_strategy() == "tagged"
+
+
+def test_context_strategy_host_side(rs):
+    """RS_STRATEGY_CONTEXT is built for 4-byte elements and the
+    sequential scheduler; other combinations fail at create time (no GPU needed)."""
+    import synth
+    p = rs.Pipeline(synth.sweep_stages(3), "sum_i64", strategy="context")
+    assert p.last_strategy() == "context"
+    assert p.workspace_bytes(100, 10000) > 0
+    with pytest.raises(rs.RSError) as e:
+        rs.Pipeline(synth.text_stages(), "count_xor64", strategy="context")
+    assert e.value.status == rs.RS_ERR_UNSUPPORTED
+    with pytest.raises(rs.RSError) as e:
+        rs.Pipeline(synth.sweep_stages(2), "sum_i64", strategy="context", flags=rs.RS_FLAG_WARP_SPECIALIZED)
+    assert e.value.status == rs.RS_ERR_UNSUPPORTED
