@@ -350,20 +350,23 @@ def run_ours(args):
         oh = torch.empty(off.shape, dtype=off.dtype, pin_memory=True)
         oh.copy_(off)
         outh = torch.empty(out[0].shape, dtype=out[0].dtype, pin_memory=True)
-        p.run_host(vh, oh, outh)          # warm-up (device buffers allocated here)
+        outh1 = (torch.empty(out[1].shape, dtype=out[1].dtype, pin_memory=True)
+                 if out[1] is not None else None)          # two-output aggregates (count+min, count+xor)
+        p.run_host(vh, oh, outh, outh1)   # warm-up (device buffers allocated here)
         k = max(1, min(args.steps, 3))
         torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(k):
-            p.run_host(vh, oh, outh)
+            p.run_host(vh, oh, outh, outh1)
         b.record(stream)
         torch.cuda.synchronize()
         e2e_ms = a.elapsed_time(b) / k
         e2e = {"value": n * world / (e2e_ms / 1e3), "unit": "items/s",
                "h2d_bytes_per_step": int(vals.numel() * vals.element_size() + off.numel() * 8),
-               "d2h_bytes_per_step": int(out[0].numel() * out[0].element_size()), "ms_per_step": e2e_ms}
+               "d2h_bytes_per_step": int(sum(o.numel() * o.element_size() for o in out if o is not None)),
+               "ms_per_step": e2e_ms}
         ok = torch.equal(outh, out[0].cpu())
         if not ok:
             e2e["mismatch"] = True
