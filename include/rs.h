@@ -87,7 +87,7 @@ typedef enum {
     RS_STRATEGY_CONTEXT = 3, /* per-lane context (§8 f2): one boundary signal {key,
                                 stamp} per region, ensembles run across boundaries, every lane
                                 computes its own region; no tags in the queues.  4-byte
-                                elements, sequential scheduler (signal_cap 0 = 64; a fuller
+                                elements, sequential scheduler (signal_cap 0 = 32; a fuller
                                 boundary queue cuts ensembles, reading R3). */
     RS_STRATEGY_AUTO = 2     /* choice made per run, transparently (§8 f1):
                                 signal when the mean region length n_elems / n_regions is at

@@ -210,7 +210,7 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     const bool tagged_ = cfg.strategy == RS_STRATEGY_TAGGED;
     if (cfg.queue_cap == 0) cfg.queue_cap = inplace ? (tagged_ ? 16 * W : 32 * W) : (nst_ >= 2 ? 8 * W : 16 * W);
     if (cfg.signal_cap == 0)
-        cfg.signal_cap = cfg.strategy == RS_STRATEGY_CONTEXT ? 64 : (inplace ? 32 : (nst_ >= 2 ? 64 : 128));
+        cfg.signal_cap = inplace ? 32 : (nst_ >= 2 ? 64 : 128);   // (context strategy: profiles/r1_tuning.txt)
     if (cfg.q0_stage == 0)
         cfg.q0_stage = inplace ? (tagged_ ? 512 : 1024) : ((tagged_ || nst_ >= 2) ? 256 : 512);
     if (!is_pow2(cfg.queue_cap) || cfg.queue_cap < 2 * W || cfg.queue_cap > 65536)
