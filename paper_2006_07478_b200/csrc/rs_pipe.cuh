@@ -908,7 +908,42 @@ struct Pipe {
     __device__ __forceinline__ void fused_run(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                               uint32_t nens, const Op op) {
         if constexpr (!TAG) fused_full(in, imask, h, nens, op);
-        else for (uint32_t k = 0; k < nens; ++k) agg_tagged(in, tin, imask, h + k * W, W, op);
+        else
+            for (uint32_t k = 0; k < nens; ++k) {
+                if constexpr (AT::heavy)
+                    if (tagged_heavy_run(in, tin, imask, h + k * W, op)) continue;
+                agg_tagged(in, tin, imask, h + k * W, W, op);
+            }
+    }
+
+    // Tagged strategy, heavy aggregate (the text hash): a full ensemble whose
+    // items all continue the carry region folds like the signal strategy's
+    // fused node -- survivors are sparse, so only each lane's first and second
+    // survivor are lifted under warp-uniform guards (fold_kept) instead of a
+    // predicated hash per slot.  Returns false (nothing consumed) otherwise.
+    template <class Op>
+    __device__ __forceinline__ bool tagged_heavy_run(const uint32_t *in, const uint32_t *tin, uint32_t imask,
+                                                     uint32_t h, const Op op) {
+        bool same = akey != 0xffffffffu;
+#pragma unroll
+        for (int j = 0; j < IPL; ++j) same = same && tin[(h + 32 * j + lane) & imask] == akey;
+        if (!__all_sync(kFull, same)) return false;
+        if constexpr (U8) {
+            if (__any_sync(kFull, dkey != akey)) {
+                const long long d = part_delta(akey);
+                dkey = akey;
+                adelta = d;
+            }
+        }
+        uint32_t v[IPL], km = 0;
+#pragma unroll
+        for (int j = 0; j < IPL; ++j) {
+            v[j] = agg_load(in, h + 32 * j + lane, imask);
+            km |= op(v[j]) ? 1u << j : 0u;
+        }
+        if constexpr (NA) fkept += __popc(km);
+        acc = fold_kept<AT>(acc, v, km, adelta);
+        return true;
     }
 
     template <int n>
