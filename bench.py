@@ -242,23 +242,6 @@ def traffic_for(workload, strategy):
     return None
 
 
-def time_pipeline(p, vals, off, out, ws, steps, warmup, torch):
-    stream = torch.cuda.current_stream()
-    for _ in range(warmup):
-        p.run(vals, off, out, ws)
-    torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    main_ms = []
-    for a, b in ev:
-        a.record(stream)
-        p.run(vals, off, out, ws)
-        b.record(stream)
-        main_ms.append(p.kernel_times()[1])
-    torch.cuda.synchronize()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    return step_ms, main_ms
-
-
 def lane_stats(st):
     res = []
     for n in range(1, st.shape[0]):

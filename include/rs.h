@@ -90,9 +90,12 @@ typedef enum {
                                 elements, sequential scheduler (signal_cap 0 = 32; a fuller
                                 boundary queue cuts ensembles, reading R3). */
     RS_STRATEGY_AUTO = 2     /* choice made per run, transparently (§8 f1):
-                                signal when the mean region length n_elems / n_regions is at
-                                least cfg.auto_min_len, else tagged.  Both strategies give
-                                bit-identical integer aggregates, so the choice only
+                                signal when the call's mean region length
+                                (d_offsets[n_regions] - d_offsets[0]) / n_regions is at least
+                                cfg.auto_min_len, else tagged.  Decided on the device by the
+                                prepass (no host synchronisation): both strategies' kernels are
+                                enqueued and the one not chosen exits at once.  Both strategies
+                                give bit-identical integer aggregates, so the choice only
                                 moves time.  rs_pipeline_last_strategy reports it. */
 } rs_strategy;
 
@@ -108,17 +111,15 @@ enum {
     RS_FLAG_VALIDATE = 2u,   /* device-check offsets monotone and <= n_elems          */
     RS_FLAG_TIMING = 4u,     /* record CUDA events around each kernel of a run        */
     RS_FLAG_PROFILE = 16u,   /* per-node clock64() cycle counters (rs_pipeline_profile)  */
-    RS_FLAG_WARP_SPECIALIZED = 8u, /* one CTA per instance with one warp per node, nodes
-                                      running concurrently (signals carry emission positions),
-                                      instead of the default one-warp instance whose scheduler
-                                      fires one node at a time */
+    RS_FLAG_RESERVED8 = 8u,  /* round 1's warp-specialised scheduler (removed: slower than the
+                                sequential one); create rejects it with RS_ERR_UNSUPPORTED */
     RS_FLAG_UNFUSED = 32u    /* sequential scheduler: keep the AGGREGATE as a separate node
                                 with its own queue (the paper's node structure).
                                 Default: the aggregate is folded into the last FILTER/
                                 TRANSFORM node, which adds its surviving items straight into
                                 the per-region accumulator (same results; the AGGREGATE's
-                                stats then report that node's firings).  No effect with
-                                RS_FLAG_WARP_SPECIALIZED or without stages. */
+                                stats then report that node's firings).  No effect without
+                                stages. */
 };
 
 typedef struct {
@@ -128,8 +129,8 @@ typedef struct {
                                 sequential scheduler: all queues share ONE in-place ring of
                                 max(4*q0_stage, min(queue_cap, 8*q0_stage)) items, raised to fit one
                                 partial ensemble per queue plus a stage (0 = auto: 32w signal, 16w
-                                tagged).  u8 elements or RS_FLAG_WARP_SPECIALIZED: capacity of each
-                                inter-stage queue (0 = auto: 8w with 2+ stages, else 16w). */
+                                tagged).  u8 elements: capacity of each inter-stage queue
+                                (0 = auto: 8w with 2+ stages, else 16w). */
     uint32_t signal_cap;     /* signal queue capacity (entries, power of 2, >= 4; 0 = auto) */
     int32_t grid;            /* persistent CTAs; 0 = fill the device                  */
     uint32_t chunk;          /* children per parent-stream claim; 0 = default        */
@@ -227,7 +228,8 @@ rs_status rs_pipeline_geometry(const rs_pipeline *p, int32_t *grid, int32_t *war
                                int32_t *chunk);
 
 /* Strategy the last run used (RS_STRATEGY_SIGNAL or RS_STRATEGY_TAGGED; for an
- * AUTO pipeline that has not run yet, RS_STRATEGY_AUTO).  Host only. */
+ * AUTO pipeline that has not run yet, RS_STRATEGY_AUTO).  For an AUTO pipeline
+ * this reads the device's decision and synchronises the last run's stream. */
 rs_status rs_pipeline_last_strategy(const rs_pipeline *p, int32_t *strategy);
 
 void rs_pipeline_destroy(rs_pipeline *p);

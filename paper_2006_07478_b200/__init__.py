@@ -25,7 +25,7 @@ OPS = {"none": 0, "hash_lt": 1, "lt_u32": 2, "class": 3, "scale_f32": 10, "affin
 DTYPES = {"i32": 0, "u32": 1, "u8": 2, "f32": 3}
 STRATEGIES = {"signal": 0, "tagged": 1, "auto": 2, "context": 3}
 STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
-RS_FLAG_STATS, RS_FLAG_VALIDATE, RS_FLAG_TIMING, RS_FLAG_WARP_SPECIALIZED, RS_FLAG_PROFILE, RS_FLAG_UNFUSED = 1, 2, 4, 8, 16, 32
+RS_FLAG_STATS, RS_FLAG_VALIDATE, RS_FLAG_TIMING, RS_FLAG_RESERVED8, RS_FLAG_PROFILE, RS_FLAG_UNFUSED = 1, 2, 4, 8, 16, 32
 
 EXPORTS = ["rs_config_default", "rs_pipeline_create", "rs_pipeline_workspace_bytes", "rs_pipeline_run",
            "rs_pipeline_run_host", "rs_pipeline_stats", "rs_pipeline_profile", "rs_pipeline_check",

@@ -1,6 +1,6 @@
 // rs.cu — the C ABI of include/rs.h (host side of the B200 pipeline).
 //
-// Kernels live in rs_kern.cuh / rs_pipe.cuh / rs_ws.cuh and are instantiated per
+// Kernels live in rs_kern.cuh / rs_pipe.cuh and are instantiated per
 // aggregate in rs_k<AGG>.cu; see rs_kern.cuh for the execution model.
 #define RS_HOST_ONLY
 #include "rs_kern.cuh"
@@ -10,6 +10,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 using namespace rsk;
 
@@ -46,25 +47,31 @@ struct rs_pipeline {
     size_t h_dbuf_bytes = 0;
     // RS_STRATEGY_AUTO: one pipeline per strategy, the run picks (§8 f1)
     rs_pipeline *sub[2] = {nullptr, nullptr};
-    rs_pipeline *last = nullptr;
     uint32_t auto_min_len = 0;
+    cudaStream_t last_stream = nullptr;
 };
 
 namespace {
 
-// AUTO pipelines: the sub-pipeline a run uses (mean region length vs the
-// crossover), and the one queries refer to (the last run's).
-rs_pipeline *choose(rs_pipeline *p, int64_t n_elems, int64_t n_regions) {
-    if (!p->sub[0]) return p;
-    const bool sig = n_regions > 0 && (double)n_elems >= (double)p->auto_min_len * (double)n_regions;
-    p->last = p->sub[sig ? 0 : 1];
-    return p->last;
+// Process-wide: the dynamic shared-memory limit of a kernel is a per-function
+// attribute, so it is raised once per (kernel, device) to the opt-in maximum
+// under a lock; launches and occupancy probes then only ever ask for less
+// (per-run re-setting raced between handles on different threads).
+std::mutex g_attr_mu;
+bool ensure_smem_attr(KernelFn f, int dev) {
+    static std::vector<std::pair<KernelFn, int>> done;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    for (auto &d : done)
+        if (d.first == f && d.second == dev) return true;
+    int optin = 0;
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return false;
+    if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    done.push_back({f, dev});
+    return true;
 }
-const rs_pipeline *route(const rs_pipeline *p) {
-    if (!p || !p->sub[0]) return p;
-    return p->last ? p->last : p->sub[0];
-}
-rs_pipeline *route(rs_pipeline *p) { return const_cast<rs_pipeline *>(route(static_cast<const rs_pipeline *>(p))); }
 
 // Crossover region length (children per region) above which the signal
 // strategy beats tagged on B200, by FILTER/TRANSFORM stage count
@@ -163,8 +170,6 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
         case RS_OP_COUNT_MIN_U32: if (elem != RS_U32) return fail(RS_ERR_UNSUPPORTED, "COUNT_MIN_U32 needs u32 elements"); break;
         case RS_OP_COUNT_XOR64:
             if (elem != RS_U8) return fail(RS_ERR_UNSUPPORTED, "COUNT_XOR64 needs u8 elements");
-            if (cfg_in && (cfg_in->flags & RS_FLAG_WARP_SPECIALIZED))
-                return fail(RS_ERR_UNSUPPORTED, "COUNT_XOR64 is built for the sequential scheduler only");
             break;
         default: return fail(RS_ERR_UNSUPPORTED, "unknown aggregate op");
     }
@@ -194,8 +199,10 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     if (cfg.strategy != RS_STRATEGY_SIGNAL && cfg.strategy != RS_STRATEGY_TAGGED && cfg.strategy != RS_STRATEGY_CONTEXT)
         return fail(RS_ERR_INVALID_ARG, "bad strategy");
     const bool ctx_ = cfg.strategy == RS_STRATEGY_CONTEXT;
-    if (ctx_ && (elem == RS_U8 || (cfg.flags & RS_FLAG_WARP_SPECIALIZED)))
-        return fail(RS_ERR_UNSUPPORTED, "the context strategy is built for 4-byte elements and the sequential scheduler");
+    if (ctx_ && elem == RS_U8)
+        return fail(RS_ERR_UNSUPPORTED, "the context strategy is built for 4-byte elements");
+    if (cfg.flags & RS_FLAG_RESERVED8)
+        return fail(RS_ERR_UNSUPPORTED, "flag 8 (the round-1 warp-specialised scheduler) was removed");
     if (cfg.simd_width == 0) cfg.simd_width = W;
     if (cfg.simd_width != (uint32_t)W) return fail(RS_ERR_UNSUPPORTED, "only simd_width 128 is built");
     // Defaults tuned on B200 (profiles/r1_tuning.txt): deep queues amortise the
@@ -205,8 +212,8 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     // In-place pipelines (4-byte elements, sequential scheduler): all queues
     // share one ring of queue_cap items fed by TMA stages of q0_stage; a big
     // ring amortises the scheduler, the tag ring doubles the tagged footprint
-    // (profiles/r1_tuning.txt, tools/tune4.py).
-    const bool inplace = elem != RS_U8 && !(cfg.flags & RS_FLAG_WARP_SPECIALIZED);
+    // (profiles/r1_tuning.txt).
+    const bool inplace = elem != RS_U8;
     const bool tagged_ = cfg.strategy == RS_STRATEGY_TAGGED;
     if (cfg.queue_cap == 0) cfg.queue_cap = inplace ? (tagged_ ? 16 * W : 32 * W) : (nst_ >= 2 ? 8 * W : 16 * W);
     if (cfg.signal_cap == 0)
@@ -284,6 +291,74 @@ rs_status rs_pipeline_workspace_bytes(const rs_pipeline *p, int64_t n_regions, i
     return RS_OK;
 }
 
+// Geometry and kernel parameters of one (non-AUTO) pipeline for a run.
+struct Prep {
+    Launch L;
+    KParams K;
+    WsLayout wl;
+    uint32_t cta_smem;
+};
+
+static rs_status prepare(rs_pipeline *p, const void *d_elems, int64_t n_elems, const int64_t *d_offsets,
+                         int64_t n_regions, rs_aggregates out, void *d_ws, size_t ws_bytes, Prep &pr) {
+    Launch &L = pr.L;
+    if (!get_launch(p, &L)) return fail(RS_ERR_UNSUPPORTED, "aggregate not built");
+    if (!out.v0 || (L.out_bytes1 && !out.v1)) return fail(RS_ERR_INVALID_ARG, "output array is NULL");
+    pr.wl = layout(p, n_regions, n_elems, L);
+    if (!d_ws || ws_bytes < pr.wl.total) return fail(RS_ERR_WORKSPACE, "workspace smaller than rs_pipeline_workspace_bytes");
+    if (((uintptr_t)d_ws & 255u) != 0) return fail(RS_ERR_WORKSPACE, "workspace must be 256-byte aligned");
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(RS_ERR_CUDA, "cudaGetDevice failed");
+    if (!ensure_smem_attr(L.main, dev)) return fail(RS_ERR_CUDA, "cannot raise the kernel's shared-memory limit");
+    if (p->device != dev || p->grid == 0) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        // one instance per warp; pick warps-per-CTA to pack the most instances per SM
+        int best = 0, best_w = 1;
+        for (int w = WPB_MAX; w >= 1; --w) {
+            const uint32_t bytes = L.inst_bytes * w;
+            int per_sm = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.main, w * 32, bytes) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
+            if (per_sm * w > best) { best = per_sm * w; best_w = w; }
+        }
+        if (best < 1) return fail(RS_ERR_UNSUPPORTED, "pipeline does not fit on an SM (queue/signal capacities too large)");
+        p->wpb = best_w;
+        p->grid = p->cfg.grid > 0 ? p->cfg.grid : sms * (best / best_w);
+        p->device = dev;
+    }
+    pr.cta_smem = L.inst_bytes * p->wpb;
+
+    KParams &K = pr.K;
+    std::memset(&K, 0, sizeof K);
+    K.elems = (const uint8_t *)d_elems;
+    K.n_elems = n_elems;
+    K.off = (const long long *)d_offsets;
+    K.R = n_regions;
+    K.out0 = out.v0;
+    K.out1 = out.v1;
+    uint8_t *ws = (uint8_t *)d_ws;
+    K.hdr = (WsHdr *)(ws + pr.wl.hdr);
+    K.stats = (unsigned long long *)(ws + pr.wl.stats);
+    K.chunk_fr = (uint32_t *)(ws + pr.wl.fr);
+    K.part0 = ws + pr.wl.part0;
+    K.part1 = ws + pr.wl.part1;
+    K.max_chunks = pr.wl.max_chunks;
+    K.C = p->cfg.chunk;
+    K.qcap = p->cfg.queue_cap;
+    K.scap = p->cfg.signal_cap;
+    K.q0_stage = p->cfg.q0_stage;
+    K.ring0 = L.ring0;
+    K.esize = p->elem == RS_U8 ? 1u : 4u;
+    K.flags = p->cfg.flags;
+    K.tagged = p->cfg.strategy == RS_STRATEGY_TAGGED;
+    K.nst = p->nst;
+    std::memcpy(K.st, p->st, sizeof K.st);
+    return RS_OK;
+}
+
 static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, const int64_t *d_offsets,
                           int64_t n_regions, rs_aggregates out, void *d_ws, size_t ws_bytes, cudaStream_t stream) {
     if (!p) return fail(RS_ERR_INVALID_ARG, "pipeline is NULL");
@@ -295,94 +370,45 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
     if (n_elems > 0 && !d_elems) return fail(RS_ERR_INVALID_ARG, "d_elems is NULL");
     if (((uintptr_t)d_elems & 15u) != 0) return fail(RS_ERR_INVALID_ARG, "d_elems must be 16-byte aligned");
     if (((uintptr_t)d_offsets & 7u) != 0) return fail(RS_ERR_INVALID_ARG, "d_offsets must be 8-byte aligned");
-    Launch L;
-    if (!get_launch(p, &L)) return fail(RS_ERR_UNSUPPORTED, "aggregate not built");
-    if (!out.v0 || (L.out_bytes1 && !out.v1)) return fail(RS_ERR_INVALID_ARG, "output array is NULL");
-    WsLayout wl = layout(p, n_regions, n_elems, L);
-    if (!d_ws || ws_bytes < wl.total) return fail(RS_ERR_WORKSPACE, "workspace smaller than rs_pipeline_workspace_bytes");
-    if (((uintptr_t)d_ws & 255u) != 0) return fail(RS_ERR_WORKSPACE, "workspace must be 256-byte aligned");
 
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return fail(RS_ERR_CUDA, "cudaGetDevice failed");
-    const bool seq = (p->cfg.flags & RS_FLAG_WARP_SPECIALIZED) == 0;
-    if (p->device != dev || p->grid == 0) {
-        int sms = 0;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (seq) {
-            // sequential scheduler: one instance per warp; pick warps-per-CTA to
-            // pack the most instances per SM
-            int best = 0, best_w = 1;
-            for (int w = WPB_MAX; w >= 1; --w) {
-                const uint32_t bytes = L.inst_bytes * w;
-                if (cudaFuncSetAttribute(L.main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
-                    cudaGetLastError();
-                    continue;
-                }
-                int per_sm = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.main, w * 32, bytes);
-                if (per_sm * w > best) { best = per_sm * w; best_w = w; }
-            }
-            if (best < 1) return fail(RS_ERR_UNSUPPORTED, "pipeline does not fit on an SM (queue/signal capacities too large)");
-            p->wpb = best_w;
-            p->grid = p->cfg.grid > 0 ? p->cfg.grid : sms * (best / best_w);
-        } else {
-            // warp-specialised: one instance per CTA, one warp per node
-            p->wpb = p->nst + 2;
-            if (cudaFuncSetAttribute(L.ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.ws_bytes) != cudaSuccess)
-                return fail(RS_ERR_UNSUPPORTED, "pipeline shared memory exceeds the per-CTA limit");
-            int per_sm = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.ws, p->wpb * 32, L.ws_bytes);
-            if (per_sm < 1) return fail(RS_ERR_UNSUPPORTED, "pipeline does not fit on an SM (queue/signal capacities too large)");
-            p->grid = p->cfg.grid > 0 ? p->cfg.grid : sms * per_sm;
-        }
-        p->device = dev;
+    // RS_STRATEGY_AUTO: both strategies' kernels are enqueued; the prepass
+    // decides on the device from the call's children count and the kernel of
+    // the other strategy exits at once (no host synchronisation).
+    const bool is_auto = p->sub[0] != nullptr;
+    Prep pa, pb;
+    rs_status s = prepare(is_auto ? p->sub[0] : p, d_elems, n_elems, d_offsets, n_regions, out, d_ws, ws_bytes, pa);
+    if (s != RS_OK) return s;
+    if (is_auto) {
+        s = prepare(p->sub[1], d_elems, n_elems, d_offsets, n_regions, out, d_ws, ws_bytes, pb);
+        if (s != RS_OK) return s;
+        pa.K.auto_sel = 1;
+        pb.K.auto_sel = 2;
     }
-    const uint32_t cta_smem = seq ? L.inst_bytes * p->wpb : L.ws_bytes;
-    cudaFuncSetAttribute(seq ? L.main : L.ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cta_smem);
-
-    KParams K;
-    std::memset(&K, 0, sizeof K);
-    K.elems = (const uint8_t *)d_elems;
-    K.n_elems = n_elems;
-    K.off = (const long long *)d_offsets;
-    K.R = n_regions;
-    K.out0 = out.v0;
-    K.out1 = out.v1;
-    uint8_t *ws = (uint8_t *)d_ws;
-    K.hdr = (WsHdr *)(ws + wl.hdr);
-    K.stats = (unsigned long long *)(ws + wl.stats);
-    K.chunk_fr = (uint32_t *)(ws + wl.fr);
-    K.part0 = ws + wl.part0;
-    K.part1 = ws + wl.part1;
-    K.max_chunks = wl.max_chunks;
-    K.C = p->cfg.chunk;
-    K.qcap = p->cfg.queue_cap;
-    K.scap = p->cfg.signal_cap;
-    K.q0_stage = p->cfg.q0_stage;
-    K.ring0 = L.ring0;
-    K.esize = p->elem == RS_U8 ? 1u : 4u;
-    K.flags = p->cfg.flags;
-    K.tagged = p->cfg.strategy == RS_STRATEGY_TAGGED;
-    K.nst = p->nst;
-    std::memcpy(K.st, p->st, sizeof K.st);
-
-    int pre_blocks = (int)std::min<long long>((2 * wl.max_chunks + 2 + 255) / 256, 148 * 8);
-    if (K.tagged || (K.flags & RS_FLAG_VALIDATE)) pre_blocks = std::max(pre_blocks, 148 * 8);
-    const bool timing = (K.flags & RS_FLAG_TIMING) != 0;
+    KParams Kpre = pa.K;
+    if (is_auto) {
+        Kpre.tagged = -1;
+        Kpre.auto_min_len = p->auto_min_len;
+    }
+    int pre_blocks = (int)std::min<long long>((2 * pa.wl.max_chunks + 2 + 255) / 256, 148 * 8);
+    if (Kpre.tagged || (Kpre.flags & RS_FLAG_VALIDATE)) pre_blocks = std::max(pre_blocks, 148 * 8);
+    const bool timing = (pa.K.flags & RS_FLAG_TIMING) != 0;
     if (timing && !p->ev[0])
         for (int i = 0; i < 4; ++i) cudaEventCreate(&p->ev[i]);
     p->timed = timing;
+    // header (claim cursor, error word, strategy) + stats, zeroed before any kernel reads them
+    if (cudaMemsetAsync(d_ws, 0, pa.wl.fr, stream) != cudaSuccess) return fail(RS_ERR_CUDA, "workspace reset failed");
     if (timing) cudaEventRecord(p->ev[0], stream);
-    L.pre<<<pre_blocks, 256, 0, stream>>>(K, 4 * (MAXK + 2) + 16);
+    pa.L.pre<<<pre_blocks, 256, 0, stream>>>(Kpre);
     if (timing) cudaEventRecord(p->ev[1], stream);
-    if (seq) L.main<<<p->grid, p->wpb * 32, cta_smem, stream>>>(K);
-    else L.ws<<<p->grid, p->wpb * 32, cta_smem, stream>>>(K);
+    pa.L.main<<<(is_auto ? p->sub[0] : p)->grid, (is_auto ? p->sub[0] : p)->wpb * 32, pa.cta_smem, stream>>>(pa.K);
+    if (is_auto) pb.L.main<<<p->sub[1]->grid, p->sub[1]->wpb * 32, pb.cta_smem, stream>>>(pb.K);
     if (timing) cudaEventRecord(p->ev[2], stream);
-    int fix_blocks = (int)std::min<long long>((wl.max_chunks + 255) / 256, 148 * 8);
-    L.fix<<<std::max(fix_blocks, 1), 256, 0, stream>>>(K);
+    int fix_blocks = (int)std::min<long long>((pa.wl.max_chunks + 255) / 256, 148 * 8);
+    pa.L.fix<<<std::max(fix_blocks, 1), 256, 0, stream>>>(pa.K);
     if (timing) cudaEventRecord(p->ev[3], stream);
-    p->launches = 3;
+    p->launches = is_auto ? 4 : 3;
     p->last_ws = d_ws;
+    p->last_stream = stream;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, std::string("launch failed: ") + cudaGetErrorString(e));
     return RS_OK;
@@ -391,8 +417,7 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
 rs_status rs_pipeline_run(rs_pipeline *p, const void *d_elems, int64_t n_elems, const int64_t *d_offsets,
                           int64_t n_regions, rs_aggregates out, void *d_ws, size_t ws_bytes, rs_stream stream) {
     if (!p) return fail(RS_ERR_INVALID_ARG, "pipeline is NULL");
-    return run_impl(choose(p, n_elems, n_regions), d_elems, n_elems, d_offsets, n_regions, out, d_ws, ws_bytes,
-                    (cudaStream_t)stream);
+    return run_impl(p, d_elems, n_elems, d_offsets, n_regions, out, d_ws, ws_bytes, (cudaStream_t)stream);
 }
 
 rs_status rs_pipeline_run_host(rs_pipeline *p, const void *h_elems, int64_t n_elems, const int64_t *h_offsets,
@@ -401,7 +426,6 @@ rs_status rs_pipeline_run_host(rs_pipeline *p, const void *h_elems, int64_t n_el
     if (n_regions < 0 || n_elems < 0) return fail(RS_ERR_INVALID_ARG, "negative size");
     if (n_regions == 0) return RS_OK;
     if (!h_offsets || (n_elems > 0 && !h_elems)) return fail(RS_ERR_INVALID_ARG, "NULL host buffer");
-    if (p->sub[0]) return rs_pipeline_run_host(choose(p, n_elems, n_regions), h_elems, n_elems, h_offsets, n_regions, h_out, stream_);
     Launch L;
     if (!get_launch(p, &L)) return fail(RS_ERR_UNSUPPORTED, "aggregate not built");
     if (!h_out.v0 || (L.out_bytes1 && !h_out.v1)) return fail(RS_ERR_INVALID_ARG, "output array is NULL");
@@ -440,7 +464,6 @@ rs_status rs_pipeline_run_host(rs_pipeline *p, const void *h_elems, int64_t n_el
 }
 
 rs_status rs_pipeline_profile(rs_pipeline *p, uint64_t *host16, rs_stream stream) {
-    p = route(p);
     if (!p || !host16) return fail(RS_ERR_INVALID_ARG, "NULL argument");
     if (!p->last_ws) { std::memset(host16, 0, 16 * sizeof(uint64_t)); return RS_OK; }
     if (cudaMemcpyAsync(host16, (uint8_t *)p->last_ws + 256 + sizeof(unsigned long long) * 4 * (MAXK + 2),
@@ -451,7 +474,6 @@ rs_status rs_pipeline_profile(rs_pipeline *p, uint64_t *host16, rs_stream stream
 }
 
 rs_status rs_pipeline_stats(rs_pipeline *p, rs_node_stats *host_out, int n_nodes, rs_stream stream) {
-    p = route(p);
     if (!p || !host_out) return fail(RS_ERR_INVALID_ARG, "NULL argument");
     if (n_nodes != p->n_nodes) return fail(RS_ERR_INVALID_ARG, "n_nodes must equal the create-time node count");
     if (!p->last_ws) {
@@ -473,7 +495,6 @@ rs_status rs_pipeline_stats(rs_pipeline *p, rs_node_stats *host_out, int n_nodes
 }
 
 rs_status rs_pipeline_check(rs_pipeline *p, rs_stream stream, int32_t *code) {
-    p = route(p);
     if (!p) return fail(RS_ERR_INVALID_ARG, "NULL pipeline");
     if (code) *code = 0;
     if (!p->last_ws) return RS_OK;
@@ -487,19 +508,28 @@ rs_status rs_pipeline_check(rs_pipeline *p, rs_stream stream, int32_t *code) {
 }
 
 int rs_pipeline_launches(const rs_pipeline *p) {
-    p = route(p);
     return p ? p->launches : 0;
+}
+
+// Strategy of the last run: an AUTO handle reads the prepass's decision from
+// the workspace header (synchronises the last run's stream).
+static int32_t last_sel(const rs_pipeline *p) {
+    if (!p->sub[0]) return p->cfg.strategy;
+    if (!p->last_ws) return RS_STRATEGY_AUTO;
+    WsHdr h;
+    if (cudaMemcpyAsync(&h, p->last_ws, sizeof h, cudaMemcpyDeviceToHost, p->last_stream) != cudaSuccess ||
+        cudaStreamSynchronize(p->last_stream) != cudaSuccess)
+        return RS_STRATEGY_AUTO;
+    return h.sel ? RS_STRATEGY_TAGGED : RS_STRATEGY_SIGNAL;
 }
 
 rs_status rs_pipeline_last_strategy(const rs_pipeline *p, int32_t *strategy) {
     if (!p || !strategy) return fail(RS_ERR_INVALID_ARG, "NULL argument");
-    if (p->sub[0]) *strategy = p->last ? p->last->cfg.strategy : RS_STRATEGY_AUTO;
-    else *strategy = p->cfg.strategy;
+    *strategy = last_sel(p);
     return RS_OK;
 }
 
 rs_status rs_pipeline_kernel_times(rs_pipeline *p, float *ms3, rs_stream stream) {
-    p = route(p);
     if (!p || !ms3) return fail(RS_ERR_INVALID_ARG, "NULL argument");
     if (!p->timed || !p->ev[0]) return fail(RS_ERR_INVALID_ARG, "last run was not made with RS_FLAG_TIMING");
     if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return fail(RS_ERR_CUDA, "stream synchronize failed");
@@ -509,8 +539,8 @@ rs_status rs_pipeline_kernel_times(rs_pipeline *p, float *ms3, rs_stream stream)
 }
 
 rs_status rs_pipeline_geometry(const rs_pipeline *p, int32_t *grid, int32_t *wpb, int32_t *chunk) {
-    p = route(p);
     if (!p) return fail(RS_ERR_INVALID_ARG, "NULL pipeline");
+    if (p->sub[0]) p = p->sub[last_sel(p) == RS_STRATEGY_TAGGED ? 1 : 0];
     if (grid) *grid = p->grid;
     if (wpb) *wpb = p->wpb;
     if (chunk) *chunk = (int32_t)p->cfg.chunk;

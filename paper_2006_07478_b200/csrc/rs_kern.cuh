@@ -42,7 +42,6 @@ constexpr int MAXK = 4;             // max FILTER/TRANSFORM stages
 // RS_STRATEGY_AUTO crossover (children per region at which signal beats
 // tagged) by stage count 0..4, measured on B200 (tools/crossover.py)
 constexpr uint32_t AUTO_T0 = 128, AUTO_T1 = 256, AUTO_T2 = 512, AUTO_T3 = 768, AUTO_T4 = 2048;
-constexpr int NST = 4;              // TMA stages in the Q0 ring (warp-specialised kernel; separate-queue rings)
 constexpr int NSTMAX = 8;           // TMA stages of an in-place ring (sequential kernel)
 constexpr int WPB = 4;              // warps (instances) per CTA (default)
 constexpr int WPB_MAX = 16;         // sequential kernel: up to 16 instances per CTA (one CTA may fill an SM)
@@ -60,7 +59,7 @@ struct WsHdr {
     uint32_t claim;      // parent-stream cursor (chunks)
     int32_t err;         // first device error
     uint32_t nchunks;
-    uint32_t pad_;
+    int32_t sel;         // strategy the run uses (0 signal, 1 tagged; RS_STRATEGY_AUTO decides on the device)
     long long base0;     // align_down(offsets[0], 16 bytes)
     long long off0, offR;
 };
@@ -82,7 +81,9 @@ struct KParams {
     uint32_t ring0;                 // Q0 ring capacity in elements (sequential kernel; in-place: all queues)
     uint32_t esize;                 // element size in bytes (1 = u8 text, else 4)
     uint32_t flags;
-    int32_t tagged;
+    int32_t tagged;                 // 1 tagged; -1 = AUTO (the prepass decides, see k_prepass)
+    int32_t auto_sel;               // AUTO: 0 always run; 1 = run iff hdr->sel == 0; 2 = iff hdr->sel == 1
+    uint32_t auto_min_len;          // AUTO: signal iff children >= auto_min_len * regions
     int32_t nst;
     StageP st[MAXK];
 };
@@ -103,11 +104,16 @@ __device__ __forceinline__ bool stage_apply(const StageP &s, uint32_t &v) {
 // --------------------------------------------------------------- prepass
 // Chunk boundaries: b_0 = off0, b_k = base0 + k*C; chunk_fr[k] = first region
 // r with off[r] >= b_k (lower bound over off[0..R-1]); chunk_fr[nchunks] = R.
-// Also resets the claim counter / error word / stats, initialises partial
-// slots to the identity and (tagged strategy) the outputs to the identity
-// (A1: regions none of whose items reach the aggregate report identity).
+// Also initialises partial slots to the identity and (tagged strategy) the
+// outputs to the identity (A1: regions none of whose items reach the
+// aggregate report identity).  The header words it depends on (claim, err,
+// stats) were zeroed by a memset enqueued before it, so the VALIDATE CASes of
+// any block cannot race with a reset.
+// RS_STRATEGY_AUTO (P.tagged < 0): every thread derives the same decision from
+// the call's own children count off[R] - off[0] (not the array bound n_elems,
+// which may cover a larger stream), so no cross-block communication is needed.
 template <int AGG>
-__global__ void k_prepass(KParams P, int n_stats) {
+__global__ void k_prepass(KParams P) {
     using AT = AggT<AGG>;
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nth = (long long)gridDim.x * blockDim.x;
@@ -119,15 +125,16 @@ __global__ void k_prepass(KParams P, int n_stats) {
     long long nch = span <= 0 ? 1 : (span + P.C - 1) / P.C;
     bool bad = nch > P.max_chunks || offR < off0 || off0 < 0 || offR > P.n_elems;
     if (bad) nch = 0;
+    bool tagged = P.tagged > 0;
+    if (P.tagged < 0) tagged = !bad && (double)(offR - off0) < (double)P.auto_min_len * (double)P.R;
     if (tid == 0) {
-        P.hdr->claim = 0;
-        P.hdr->err = bad ? ERR_OFFSETS : 0;
+        if (bad) atomicCAS((int *)&P.hdr->err, 0, ERR_OFFSETS);
         P.hdr->nchunks = (uint32_t)nch;
+        P.hdr->sel = tagged ? 1 : 0;
         P.hdr->base0 = base0;
         P.hdr->off0 = off0;
         P.hdr->offR = offR;
     }
-    for (long long i = tid; i < n_stats; i += nth) P.stats[i] = 0ull;
     for (long long k = tid; k <= nch; k += nth) {
         uint32_t fr;
         if (k == nch) {
@@ -144,12 +151,11 @@ __global__ void k_prepass(KParams P, int n_stats) {
         P.chunk_fr[k] = fr;
     }
     for (long long s = tid; s < 2 * nch; s += nth) AT::store(P.part0, P.part1, (uint64_t)s, AT::id());
-    if (P.tagged)
+    if (tagged)
         for (long long r = tid; r < P.R; r += nth) AT::store(P.out0, P.out1, (uint64_t)r, AT::id());
     if (P.flags & RS_FLAG_VALIDATE) {
         for (long long r = tid; r < P.R; r += nth)
             if (P.off[r + 1] < P.off[r]) atomicCAS((int *)&P.hdr->err, 0, ERR_OFFSETS);
-        if (tid == 0 && (offR > P.n_elems || off0 < 0)) atomicCAS((int *)&P.hdr->err, 0, ERR_OFFSETS);
     }
 }
 
@@ -184,16 +190,13 @@ __global__ void k_fixup(KParams P) {
 // ---------------------------------------------------------- the pipeline
 #ifndef RS_HOST_ONLY
 #include "rs_pipe.cuh"
-#include "rs_ws.cuh"
 #endif
 
 using KernelFn = void (*)(KParams);
 
 struct Launch {
     KernelFn main;
-    KernelFn ws;
-    uint32_t ws_bytes;
-    void (*pre)(KParams, int);
+    void (*pre)(KParams);
     void (*fix)(KParams);
     uint32_t inst_bytes;
     uint32_t ring0;                 // Q0 ring capacity (elements) of the sequential kernel
@@ -215,28 +218,6 @@ KernelFn pick_k(int K) {
         case 2: return k_pipeline<2, AGG, TAG, FUSE, CTX>;
         case 3: return k_pipeline<3, AGG, TAG, FUSE, CTX>;
         default: return k_pipeline<4, AGG, TAG, FUSE, CTX>;
-    }
-}
-
-template <int AGG, bool TAG>
-KernelFn pick_ws(int K) {
-    switch (K) {
-        case 0: return k_pipeline_ws<0, AGG, TAG>;
-        case 1: return k_pipeline_ws<1, AGG, TAG>;
-        case 2: return k_pipeline_ws<2, AGG, TAG>;
-        case 3: return k_pipeline_ws<3, AGG, TAG>;
-        default: return k_pipeline_ws<4, AGG, TAG>;
-    }
-}
-
-template <int AGG, bool TAG>
-uint32_t smem_ws(int K, uint32_t qcap, uint32_t scap) {
-    switch (K) {
-        case 0: return WS<0, AGG, TAG>::smem_bytes(qcap, scap);
-        case 1: return WS<1, AGG, TAG>::smem_bytes(qcap, scap);
-        case 2: return WS<2, AGG, TAG>::smem_bytes(qcap, scap);
-        case 3: return WS<3, AGG, TAG>::smem_bytes(qcap, scap);
-        default: return WS<4, AGG, TAG>::smem_bytes(qcap, scap);
     }
 }
 
@@ -278,8 +259,6 @@ Launch launch_for(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint
     }
     L.main = tag ? (fuse ? pick_k<AGG, true, true>(K) : pick_k<AGG, true, false>(K))
                  : (fuse ? pick_k<AGG, false, true>(K) : pick_k<AGG, false, false>(K));
-    L.ws = tag ? pick_ws<AGG, true>(K) : pick_ws<AGG, false>(K);
-    L.ws_bytes = tag ? smem_ws<AGG, true>(K, qcap, scap) : smem_ws<AGG, false>(K, qcap, scap);
     L.pre = k_prepass<AGG>;
     L.fix = k_fixup<AGG>;
     L.ring0 = tag ? (fuse ? ring_for<AGG, true, true>(K, sblk, qcap) : ring_for<AGG, true, false>(K, sblk, qcap))

@@ -65,7 +65,7 @@ __device__ __forceinline__ void filter_slices(const uint32_t *in, const uint32_t
                                               uint32_t *out, uint32_t *tout, uint32_t qmask, uint32_t &tl,
                                               const Op &op, uint32_t lt, uint32_t cmask) {
     // Masked ring addressing only (no wrap-free fast path): the smaller code
-    // measured faster than the dual-path variant (tools/ab.py, profiles/).
+    // measured faster than the dual-path variant (profiles/r1_tuning.txt).
     const uint32_t lane = threadIdx.x & 31u;
     uint32_t v[NS], tg[NS];
     bool keep[NS];
@@ -1343,7 +1343,7 @@ struct Pipe {
     }
 
     // Scheduler state of a stuck instance (workspace bytes [64, 256), read by
-    // tools/dbg_ctx.py): per edge qh, qt, sh, st, q_start, head signal word.
+    // a debugger): per edge qh, qt, sh, st, q_start, head signal word.
     template <int e = 0>
     __device__ __forceinline__ void dump_edges(uint32_t *d) {
         if constexpr (e <= K && e < 4) {
@@ -1618,6 +1618,7 @@ __global__ void __launch_bounds__(WPB_MAX * 32, 1) k_pipeline(const __grid_const
     using PP = Pipe<K, AGG, TAG, FUSE, CTX>;
     uint8_t *mine = smem + (size_t)warp * PP::smem_bytes(P.qcap, P.scap, P.ring0);
     if (P.hdr->err) return;
+    if (P.auto_sel && P.hdr->sel != P.auto_sel - 1) return;   // AUTO: the other strategy's kernel runs
     PP pipe(P, mine, lane);
     pipe.run();
 }

@@ -133,8 +133,8 @@ def test_auto_strategy_host_side(rs):
 
 
 def test_context_strategy_host_side(rs):
-    """RS_STRATEGY_CONTEXT is built for 4-byte elements and the
-    sequential scheduler; other combinations fail at create time (no GPU needed)."""
+    """RS_STRATEGY_CONTEXT is built for 4-byte elements; other
+    combinations, and the removed flag 8, fail at create time (no GPU needed)."""
     import synth
     p = rs.Pipeline(synth.sweep_stages(3), "sum_i64", strategy="context")
     assert p.last_strategy() == "context"
@@ -143,5 +143,5 @@ def test_context_strategy_host_side(rs):
         rs.Pipeline(synth.text_stages(), "count_xor64", strategy="context")
     assert e.value.status == rs.RS_ERR_UNSUPPORTED
     with pytest.raises(rs.RSError) as e:
-        rs.Pipeline(synth.sweep_stages(2), "sum_i64", strategy="context", flags=rs.RS_FLAG_WARP_SPECIALIZED)
+        rs.Pipeline(synth.sweep_stages(2), "sum_i64", strategy="context", flags=rs.RS_FLAG_RESERVED8)
     assert e.value.status == rs.RS_ERR_UNSUPPORTED

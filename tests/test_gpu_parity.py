@@ -31,9 +31,9 @@ def rs():
 
 
 def run_gpu(rs, vals, off, stages, agg, strategy="signal", mode="seq", **cfg):
-    # modes: "seq" (default: sequential scheduler, aggregate fused into the last
-    # stage), "unfused" (sequential, separate AGGREGATE node), "ws" (warp-specialised)
-    flags = rs.RS_FLAG_STATS | {"ws": rs.RS_FLAG_WARP_SPECIALIZED, "unfused": rs.RS_FLAG_UNFUSED}.get(mode, 0)
+    # modes: "seq" (default: aggregate fused into the last stage), "unfused"
+    # (separate AGGREGATE node, the paper's node structure)
+    flags = rs.RS_FLAG_STATS | {"unfused": rs.RS_FLAG_UNFUSED}.get(mode, 0)
     p = rs.Pipeline(stages, agg, strategy=strategy, flags=flags, **cfg)
     dev = torch.device("cuda:0")
     e = torch.from_numpy(np.ascontiguousarray(vals)).to(dev)
@@ -115,10 +115,8 @@ def _case(seed, agg, R=None, dist=None, L=None, base=None):
 
 @pytest.mark.parametrize("seed", range(24))
 @pytest.mark.parametrize("strategy", ["signal", "tagged", "context"])
-@pytest.mark.parametrize("mode", ["ws", "seq", "unfused"])
+@pytest.mark.parametrize("mode", ["seq", "unfused"])
 def test_random_parity(rs, seed, strategy, mode):
-    if strategy == "context" and mode == "ws":
-        pytest.skip("the context strategy is built for the sequential scheduler")
     agg = ["sum_i64", "sum_f32", "count_min_u32"][seed % 3]
     vals, off, stages = _case(seed, agg)
     rnd = random.Random(seed * 7 + 1)
@@ -135,11 +133,9 @@ def test_random_parity(rs, seed, strategy, mode):
 
 @pytest.mark.parametrize("strategy", ["signal", "tagged", "context"])
 @pytest.mark.parametrize("L", [1, 4, 32, 127, 128, 129, 256, 4096, 100000])
-@pytest.mark.parametrize("mode", ["ws", "seq", "unfused"])
+@pytest.mark.parametrize("mode", ["seq", "unfused"])
 def test_region_lengths(rs, strategy, L, mode):
     """Region lengths 1..4096 (north star) plus regions far longer than a chunk."""
-    if strategy == "context" and mode == "ws":
-        pytest.skip("the context strategy is built for the sequential scheduler")
     N = 1 << 18
     R = max(1, N // L)
     for dist in ("fixed", "var"):
@@ -211,15 +207,13 @@ def test_grid_and_capacity_invariance(rs):
                 dict(queue_cap=256), dict(q0_stage=128, queue_cap=256), dict(q0_stage=128, queue_cap=1024),
                 dict(q0_stage=2048, queue_cap=16384, chunk=2048)):
         for strat in ("signal", "tagged"):
-            for mode in ("ws", "seq", "unfused"):
-                if mode == "ws" and "q0_stage" in cfg:
-                    continue                 # in-place ring sizes are a sequential-kernel knob
+            for mode in ("seq", "unfused"):
                 got, _, _ = run_gpu(rs, vals, off, stages, "sum_i64", strat, mode, **cfg)
                 assert_parity(got, ref, "sum_i64")
 
 
 @pytest.mark.parametrize("R", [32, 64, 96, 128, 256, 512, 1024])
-@pytest.mark.parametrize("mode", ["ws", "seq", "unfused"])
+@pytest.mark.parametrize("mode", ["seq", "unfused"])
 def test_occupancy_closed_form_gpu(rs, R, mode):
     """One instance (grid=1), fixed regions dividing the chunk, pass-all
     stages, full-first: the aggregate's lane fraction equals R/(w ceil(R/w))
