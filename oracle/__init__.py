@@ -186,6 +186,25 @@ def brute_range(elems, offsets, r0, r1, stages, agg, o0, o1):
         raise OracleError(ERRORS.get(rc, rc))
 
 
+def brute_sharded(elems, offsets, stages, agg, threads=None):
+    """The plain per-region fold of :func:`brute`, evaluated on `threads`
+    contiguous region shards in parallel (regions are independent contexts,
+    P:71-79; ctypes releases the GIL), for full-size parity checks."""
+    import concurrent.futures as cf
+    elems, offsets = _prep(elems, offsets)
+    R = offsets.size - 1
+    o0, o1 = _out_arrays(agg, R)
+    threads = threads or len(os.sched_getaffinity(0))
+    # shard boundaries balanced by children
+    n0, n1 = int(offsets[0]), int(offsets[-1])
+    cuts = [0] + [int(np.searchsorted(offsets[:-1], n0 + (n1 - n0) * k // threads, side="left"))
+                  for k in range(1, threads)] + [R]
+    with cf.ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda k: brute_range(elems, offsets, cuts[k], cuts[k + 1], stages, agg, o0, o1)
+                    if cuts[k + 1] > cuts[k] else None, range(threads)))
+    return o0, o1
+
+
 def node_counts(elems, offsets, stages):
     """kc[r, j] = items of region r consumed by node j+1 (j=0: first node after
     enumeration; j=len(stages): the aggregate)."""

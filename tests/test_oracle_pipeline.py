@@ -379,3 +379,28 @@ def test_empty_inputs():
 def test_bad_offsets_rejected():
     with pytest.raises(oracle.OracleError):
         oracle.brute(np.zeros(4, np.int32), np.array([0, 3, 2], np.int64), [], "sum_i64")
+
+
+# ------------------------------------------- sharded fold (full-size checks)
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_brute_sharded_prefix_identity(threads):
+    """or_brute_range / brute_sharded place every shard's regions at their
+    global indices: pinned against the numpy int64 cumsum identity
+    sum_r = P[off[r+1]] - P[off[r]] (not against brute itself), with
+    offsets[0] != 0, empty regions, and more threads than some shards need."""
+    lens = synth.lengths(3000, "zipf", seed=threads, zipf_max=500)
+    lens[::7] = 0
+    off = synth.offsets(lens, base=11)
+    vals = synth.values(int(off[-1]), "i32", seed=threads + 1)
+    P = np.concatenate([[0], np.cumsum(vals.astype(np.int64))])
+    expect = P[off[1:]] - P[off[:-1]]
+    got = oracle.brute_sharded(vals, off, [PASS_ALL], "sum_i64", threads=threads)[0]
+    np.testing.assert_array_equal(got, expect)
+    # a two-output aggregate: counts by bincount of each element's region
+    u = synth.values(int(off[-1]), "u32", seed=threads + 2)
+    cnt, mn = oracle.brute_sharded(u, off, [], "count_min_u32", threads=threads)
+    reg = np.searchsorted(off, np.arange(off[0], off[-1]), side="right") - 1
+    np.testing.assert_array_equal(cnt, np.bincount(reg, minlength=off.size - 1))
+    ref_mn = np.full(off.size - 1, 0xFFFFFFFF, np.uint64)
+    np.minimum.at(ref_mn, reg, u[off[0]:].astype(np.uint64))
+    np.testing.assert_array_equal(mn.astype(np.uint64), ref_mn)
