@@ -478,7 +478,6 @@ struct Pipe {
     __host__ static uint32_t ring_for(uint32_t sblk, uint32_t qcap) {
         uint32_t r = 4 * sblk;
         if (INPLACE) {
-            r = 2 * sblk;                 // in-place: as few as 2 stages when queue_cap asks for it
             while (r < qcap && r < NSTMAX * sblk) r <<= 1;
             while (r < (NQ + 1) * (uint32_t)W + sblk) r <<= 1;
         }
