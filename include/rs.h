@@ -113,6 +113,12 @@ enum {
     RS_FLAG_PROFILE = 16u,   /* per-node clock64() cycle counters (rs_pipeline_profile)  */
     RS_FLAG_RESERVED8 = 8u,  /* round 1's warp-specialised scheduler (removed: slower than the
                                 sequential one); create rejects it with RS_ERR_UNSUPPORTED */
+    RS_FLAG_TRACE = 64u,     /* §8(c) trace mode (SUM_I64, signal strategy only; needs
+                                rs_pipeline_set_trace): every node logs the Begin/End signals
+                                it consumes and each ensemble it fires (count, smallest and
+                                largest item value), in order, so a host checker can verify
+                                bracketing, unmixed ensembles and per-bracket counts.  A
+                                separate kernel instantiation: no cost when off. */
     RS_FLAG_UNFUSED = 32u    /* sequential scheduler: keep the AGGREGATE as a separate node
                                 with its own queue (the paper's node structure).
                                 Default: the aggregate is folded into the last FILTER/
@@ -231,6 +237,21 @@ rs_status rs_pipeline_geometry(const rs_pipeline *p, int32_t *grid, int32_t *war
  * AUTO pipeline that has not run yet, RS_STRATEGY_AUTO).  For an AUTO pipeline
  * this reads the device's decision and synchronises the last run's stream. */
 rs_status rs_pipeline_last_strategy(const rs_pipeline *p, int32_t *strategy);
+
+/* Trace buffer for RS_FLAG_TRACE runs (Lemma 1, §3.3;
+ * SURVEY §8(c) "GPU trace-mode check").  d_trace: caller-owned device buffer
+ * of `bytes` (16-byte aligned, >= 64; NULL detaches).  Every traced run first
+ * zeroes word 0 and then fills:
+ *   word 0        number of events the kernel tried to write (> capacity =
+ *                 overflow; capacity = (bytes - 32) / 32)
+ *   words 8 + 8i  event i, 8 x uint32: instance (warp) id, per-instance
+ *                 sequence number, node | type << 8 (type 1 = ENSEMBLE,
+ *                 2 = BEGIN, 3 = END; node 1..K+1, the fused last stage
+ *                 logs under its own index), region key (bit 31 = partial
+ *                 slot of a region split across chunks), resolved region id
+ *                 (BEGIN/END), item count, min item, max item (ENSEMBLE).
+ * Events of one instance are in the order the instance performed them. */
+rs_status rs_pipeline_set_trace(rs_pipeline *p, void *d_trace, uint64_t bytes);
 
 void rs_pipeline_destroy(rs_pipeline *p);
 

@@ -26,12 +26,15 @@ DTYPES = {"i32": 0, "u32": 1, "u8": 2, "f32": 3}
 STRATEGIES = {"signal": 0, "tagged": 1, "auto": 2, "context": 3}
 STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
 RS_FLAG_STATS, RS_FLAG_VALIDATE, RS_FLAG_TIMING, RS_FLAG_RESERVED8, RS_FLAG_PROFILE, RS_FLAG_UNFUSED = 1, 2, 4, 8, 16, 32
+RS_FLAG_TRACE = 64
+TRACE_ENSEMBLE, TRACE_BEGIN, TRACE_END = 1, 2, 3
 
 EXPORTS = ["rs_config_default", "rs_pipeline_create", "rs_pipeline_workspace_bytes", "rs_pipeline_run",
            "rs_pipeline_run_host", "rs_pipeline_stats", "rs_pipeline_profile", "rs_pipeline_check",
            "rs_pipeline_kernel_times",
            "rs_pipeline_launches", "rs_pipeline_last_strategy",
-           "rs_pipeline_geometry", "rs_pipeline_destroy", "rs_status_string", "rs_last_error"]
+           "rs_pipeline_geometry", "rs_pipeline_set_trace", "rs_pipeline_destroy", "rs_status_string",
+           "rs_last_error"]
 
 
 class RSError(RuntimeError):
@@ -86,6 +89,8 @@ def lib():
         L.rs_pipeline_launches.restype = i32
         L.rs_pipeline_last_strategy.argtypes = [vp, C.POINTER(C.c_int32)]
         L.rs_pipeline_geometry.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        L.rs_pipeline_set_trace.argtypes = [vp, vp, C.c_uint64]
+        L.rs_pipeline_set_trace.restype = i32
         L.rs_pipeline_destroy.argtypes = [vp]
         L.rs_pipeline_destroy.restype = None
         L.rs_status_string.argtypes = [i32]
@@ -270,6 +275,23 @@ class Pipeline:
         ms = (C.c_float * 3)()
         _check(lib().rs_pipeline_kernel_times(self.h, ms, C.c_void_p(s)))
         return [ms[0], ms[1], ms[2]]
+
+    def set_trace(self, buf):
+        """RS_FLAG_TRACE: attach a device uint8/int32 tensor as the event buffer (rs.h)."""
+        self._trace = buf
+        _check(lib().rs_pipeline_set_trace(self.h, buf.data_ptr() if buf is not None else None,
+                                           buf.numel() * buf.element_size() if buf is not None else 0))
+
+    def read_trace(self):
+        """Events of the last traced run as a uint32 array [n, 8] (see rs.h);
+        raises if the buffer overflowed."""
+        import numpy as np
+        w = self._trace.cpu().numpy().view(np.uint32)
+        n = int(w[0])
+        cap = (w.size - 8) // 8
+        if n > cap:
+            raise RuntimeError(f"trace buffer overflow: {n} events, capacity {cap}")
+        return w[8:8 + 8 * n].reshape(n, 8).copy()
 
     def launches(self) -> int:
         return int(lib().rs_pipeline_launches(self.h))

@@ -49,6 +49,9 @@ struct rs_pipeline {
     rs_pipeline *sub[2] = {nullptr, nullptr};
     uint32_t auto_min_len = 0;
     cudaStream_t last_stream = nullptr;
+    // RS_FLAG_TRACE event buffer (caller-owned device memory)
+    void *trace = nullptr;
+    uint64_t trace_bytes = 0;
 };
 
 namespace {
@@ -82,6 +85,11 @@ uint32_t auto_default(int nst) {
 }
 
 bool get_launch(const rs_pipeline *p, Launch *L) {
+    if (p->cfg.flags & RS_FLAG_TRACE) {
+        *L = launch_agg20_trace(p->nst, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap,
+                                p->cfg.q0_stage);
+        return true;
+    }
     switch (p->agg) {
         case RS_OP_SUM_I64: *L = launch_agg20(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
         case RS_OP_SUM_F32: *L = launch_agg21(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
@@ -173,6 +181,8 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
             break;
         default: return fail(RS_ERR_UNSUPPORTED, "unknown aggregate op");
     }
+    if (cfg.strategy == RS_STRATEGY_AUTO && (cfg.flags & RS_FLAG_TRACE))
+        return fail(RS_ERR_UNSUPPORTED, "RS_FLAG_TRACE is built for SUM_I64 pipelines under the signal strategy");
     if (cfg.strategy == RS_STRATEGY_AUTO) {
         rs_config c = cfg;
         rs_pipeline *a = nullptr, *b = nullptr;
@@ -198,6 +208,8 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     }
     if (cfg.strategy != RS_STRATEGY_SIGNAL && cfg.strategy != RS_STRATEGY_TAGGED && cfg.strategy != RS_STRATEGY_CONTEXT)
         return fail(RS_ERR_INVALID_ARG, "bad strategy");
+    if ((cfg.flags & RS_FLAG_TRACE) && (agg != RS_OP_SUM_I64 || cfg.strategy != RS_STRATEGY_SIGNAL))
+        return fail(RS_ERR_UNSUPPORTED, "RS_FLAG_TRACE is built for SUM_I64 pipelines under the signal strategy");
     const bool ctx_ = cfg.strategy == RS_STRATEGY_CONTEXT;
     if (ctx_ && elem == RS_U8)
         return fail(RS_ERR_UNSUPPORTED, "the context strategy is built for 4-byte elements");
@@ -389,6 +401,12 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
         Kpre.tagged = -1;
         Kpre.auto_min_len = p->auto_min_len;
     }
+    if (pa.K.flags & RS_FLAG_TRACE) {
+        if (!p->trace || p->trace_bytes < 64) return fail(RS_ERR_INVALID_ARG, "RS_FLAG_TRACE needs rs_pipeline_set_trace");
+        pa.K.trace = (uint32_t *)p->trace;
+        pa.K.trace_cap = (uint32_t)std::min<uint64_t>((p->trace_bytes - 32) / 32, 0xffffffffu);
+        if (cudaMemsetAsync(p->trace, 0, 32, stream) != cudaSuccess) return fail(RS_ERR_CUDA, "trace reset failed");
+    }
     int pre_blocks = (int)std::min<long long>((2 * pa.wl.max_chunks + 2 + 255) / 256, 148 * 8);
     if (Kpre.tagged || (Kpre.flags & RS_FLAG_VALIDATE)) pre_blocks = std::max(pre_blocks, 148 * 8);
     const bool timing = (pa.K.flags & RS_FLAG_TIMING) != 0;
@@ -544,6 +562,15 @@ rs_status rs_pipeline_geometry(const rs_pipeline *p, int32_t *grid, int32_t *wpb
     if (grid) *grid = p->grid;
     if (wpb) *wpb = p->wpb;
     if (chunk) *chunk = (int32_t)p->cfg.chunk;
+    return RS_OK;
+}
+
+rs_status rs_pipeline_set_trace(rs_pipeline *p, void *d_trace, uint64_t bytes) {
+    if (!p) return fail(RS_ERR_INVALID_ARG, "NULL pipeline");
+    if (d_trace && (bytes < 64 || ((uintptr_t)d_trace & 15u)))
+        return fail(RS_ERR_INVALID_ARG, "trace buffer must be 16-byte aligned and >= 64 bytes");
+    p->trace = d_trace;
+    p->trace_bytes = d_trace ? bytes : 0;
     return RS_OK;
 }
 

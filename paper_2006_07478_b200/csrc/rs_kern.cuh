@@ -46,6 +46,7 @@ constexpr int NSTMAX = 8;           // TMA stages of an in-place ring (sequentia
 constexpr int WPB = 4;              // warps (instances) per CTA (default)
 constexpr int WPB_MAX = 16;         // sequential kernel: up to 16 instances per CTA (one CTA may fill an SM)
 
+enum : uint32_t { TR_ENSEMBLE = 1, TR_BEGIN = 2, TR_END = 3 };   // trace event types (RS_FLAG_TRACE)
 enum : int32_t { ERR_OFFSETS = 1, ERR_WATCHDOG = 2, ERR_SIGFULL = 3, ERR_UNMATCHED = 4, ERR_QFULL = 5, ERR_LIMIT = 7 };
 
 struct StageP {
@@ -86,6 +87,8 @@ struct KParams {
     uint32_t auto_min_len;          // AUTO: signal iff children >= auto_min_len * regions
     int32_t nst;
     StageP st[MAXK];
+    uint32_t *trace;                // RS_FLAG_TRACE: [0] events written, events of 8 words from word 8
+    uint32_t trace_cap;             // events the buffer holds
 };
 
 // ------------------------------------------------------------ stage ops
@@ -208,16 +211,18 @@ Launch launch_agg20(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, ui
 Launch launch_agg21(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
 Launch launch_agg22(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
 Launch launch_agg23(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
+// RS_FLAG_TRACE instantiations (SUM_I64, signal strategy; defined in rs_k20.cu)
+Launch launch_agg20_trace(int K, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk);
 
 #ifndef RS_HOST_ONLY
-template <int AGG, bool TAG, bool FUSE, bool CTX = false>
+template <int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false>
 KernelFn pick_k(int K) {
     switch (K) {
-        case 0: return k_pipeline<0, AGG, TAG, false, CTX>;      // nothing to fuse
-        case 1: return k_pipeline<1, AGG, TAG, FUSE, CTX>;
-        case 2: return k_pipeline<2, AGG, TAG, FUSE, CTX>;
-        case 3: return k_pipeline<3, AGG, TAG, FUSE, CTX>;
-        default: return k_pipeline<4, AGG, TAG, FUSE, CTX>;
+        case 0: return k_pipeline<0, AGG, TAG, false, CTX, TR>;      // nothing to fuse
+        case 1: return k_pipeline<1, AGG, TAG, FUSE, CTX, TR>;
+        case 2: return k_pipeline<2, AGG, TAG, FUSE, CTX, TR>;
+        case 3: return k_pipeline<3, AGG, TAG, FUSE, CTX, TR>;
+        default: return k_pipeline<4, AGG, TAG, FUSE, CTX, TR>;
     }
 }
 

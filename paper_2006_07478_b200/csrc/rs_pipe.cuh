@@ -323,7 +323,7 @@ struct Chunk {
 // (survivors before it), and the aggregate gives each lane the key of the last
 // boundary at or before its item -- the context computed per lane instead of
 // stored with the items.
-template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false>
+template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false>
 struct Pipe {
     using AT = AggT<AGG>;
     using A = typename AT::A;
@@ -1019,6 +1019,7 @@ struct Pipe {
             if (lim >= (uint32_t)W) {
                 // as many full ensembles as the credit / data / space allow
                 const uint32_t nens = lim / W;
+                if constexpr (TR) trace_ens(n, in, imask, E<ei>().qh, nens * W);
                 run_full<n>(in, tin, imask, E<ei>().qh, nens);
                 E<ei>().qh += nens * W;
                 if (spend) E<ei>().cur -= nens * W;
@@ -1031,6 +1032,7 @@ struct Pipe {
                 const bool bounded = spend && lim == E<ei>().cur;      // ensemble <= credit
                 const bool dr = drained && lim == arem;
                 if (bounded || dr) {
+                    if constexpr (TR) trace_ens(n, in, imask, E<ei>().qh, lim);
                     run_partial<n>(in, tin, imask, E<ei>().qh, lim);
                     E<ei>().qh += lim;
                     if (spend) E<ei>().cur -= lim;
@@ -1058,6 +1060,7 @@ struct Pipe {
                 E<ei>().xfer = false;
                 ++nsig;
                 const bool is_end = (hs.y & END_BIT) != 0;
+                if constexpr (TR) trace_event(n, is_end ? TR_END : TR_BEGIN, hs.x, 0u, 0u, 0u);
                 if constexpr (AGGN) {
                     if (!is_end) {               // a::begin: acc = identity
                         acc = AT::id();
@@ -1083,6 +1086,55 @@ struct Pipe {
         }
         __syncwarp();
         return prog;
+    }
+
+    // ------------------------------------------------- trace mode (TR)
+    // RS_FLAG_TRACE (§8(c) GPU trace-mode check): every node logs, in the
+    // order it performs them, the Begin/End signals it consumes and each
+    // ensemble it fires with the smallest and largest item value -- the test
+    // feeds elements equal to their global index, so the host can check that
+    // the events of each node form (Begin(r) ENSEMBLE* End(r))*, that every
+    // item of an ensemble lies in the open region r (no mixed ensembles,
+    // P:375-379) and that the items per bracket equal the oracle's count
+    // (Lemma 1).  Only the trace instantiations contain this code.
+    uint32_t tseq = 0;
+    __device__ __forceinline__ uint32_t region_of(uint32_t key) const {
+        if (!(key & SLOT)) return key;
+        const uint32_t slot = key & ~SLOT, k = slot >> 1;
+        return ((slot & 1u) ? P.chunk_fr[k + 1] : P.chunk_fr[k]) - 1u;
+    }
+    __device__ __forceinline__ void trace_event(uint32_t n, uint32_t type, uint32_t key, uint32_t cnt, uint32_t lo,
+                                             uint32_t hi) {
+        if (lane == 0) {
+            const uint32_t i = atomicAdd(P.trace, 1u);
+            if (i < P.trace_cap) {
+                uint32_t *e = P.trace + 8 + 8 * (size_t)i;
+                e[0] = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+                e[1] = tseq;
+                e[2] = n | (type << 8);
+                e[3] = key;
+                e[4] = type == TR_ENSEMBLE ? 0u : region_of(key);
+                e[5] = cnt;
+                e[6] = lo;
+                e[7] = hi;
+            }
+        }
+        ++tseq;
+        __syncwarp();
+    }
+    __device__ __forceinline__ void trace_ens(uint32_t n, const uint32_t *in, uint32_t imask, uint32_t h, uint32_t cnt) {
+        for (uint32_t e0 = 0; e0 < cnt; e0 += W) {
+            const uint32_t c = min((uint32_t)W, cnt - e0);
+            uint32_t lo = 0xffffffffu, hi = 0u;
+            for (uint32_t t = lane; t < c; t += 32) {
+                const uint32_t v = in[(h + e0 + t) & imask];
+                lo = min(lo, v);
+                hi = max(hi, v);
+            }
+            lo = __reduce_min_sync(kFull, lo);
+            hi = __reduce_max_sync(kFull, hi);
+            trace_event(n, TR_ENSEMBLE, 0u, c, lo, hi);
+        }
     }
 
     // ----------------------------------------------- per-lane context (CTX)
@@ -1610,12 +1662,12 @@ struct Pipe {
     }
 };
 
-template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false>
+template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false>
 __global__ void __launch_bounds__(WPB_MAX * 32, 1) k_pipeline(const __grid_constant__ KParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    using PP = Pipe<K, AGG, TAG, FUSE, CTX>;
+    using PP = Pipe<K, AGG, TAG, FUSE, CTX, TR>;
     uint8_t *mine = smem + (size_t)warp * PP::smem_bytes(P.qcap, P.scap, P.ring0);
     if (P.hdr->err) return;
     if (P.auto_sel && P.hdr->sel != P.auto_sel - 1) return;   // AUTO: the other strategy's kernel runs
