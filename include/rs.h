@@ -49,7 +49,8 @@ typedef enum {
     RS_ERR_UNSUPPORTED = -3,       /* op/dtype combination or config value not built      */
     RS_ERR_WORKSPACE = -4,         /* workspace missing or smaller than the query         */
     RS_ERR_CUDA = -5,              /* a CUDA call or launch failed                        */
-    RS_ERR_PROTOCOL = -6           /* device detected a protocol violation (rs_pipeline_check) */
+    RS_ERR_PROTOCOL = -6,          /* device detected a protocol violation (rs_pipeline_check) */
+    RS_ERR_NCCL = -7               /* NCCL unavailable or an NCCL call failed (rs_comm_*)      */
 } rs_status;
 
 /* Node kinds of the linear pipeline (§2.1; DAGs and cycles are
@@ -69,6 +70,10 @@ typedef enum {
     RS_OP_HASH_LT = 1,       /* keep iff ((uint32)v * p0) >> 24 < p1;  p0 odd, p1 in 0..256 */
     RS_OP_LT_U32 = 2,        /* keep iff (uint32)v < p1;               p1 in 0..2^32       */
     RS_OP_CLASS = 3,         /* keep iff bit v of the 32-byte bitmap `table` is set (u8)   */
+    RS_OP_PARENT_LT = 4,     /* keep iff (uint32)v < d_parent_ctx[region]: the node reads its
+                                parent object (getParent, Fig. 5).  Signal
+                                strategy only (the context is uniform over an ensemble there,
+                                P:464-465); 4-byte elements; rs_pipeline_run needs d_parent_ctx. */
     /* TRANSFORM ops */
     RS_OP_SCALE_F32 = 10,    /* v = p0_as_float * v, fp32 round-to-nearest, no FMA (f32)   */
     RS_OP_AFFINE_I32 = 11,   /* v = (uint32)(v * p0 + p1)  (i32 / u32)                     */
@@ -186,24 +191,30 @@ rs_status rs_pipeline_workspace_bytes(const rs_pipeline *p, int64_t n_regions, i
  * entries, d_offsets[0] may be > 0 so a batch or shard can address a slice of a
  * larger stream).  Empty regions are legal.  Writes exactly one
  * aggregate per region into out.v0[j] (and out.v1[j]) (A2).
- *   d_elems     device, 16-byte aligned, n_elems elements of the create-time dtype;
- *               d_offsets[n_regions] <= n_elems is required (checked on device only
- *               with RS_FLAG_VALIDATE).  May be NULL when n_elems == 0.
- *   n_regions   0 .. 2^31-1.
- *   d_ws        workspace of >= rs_pipeline_workspace_bytes(p, n_regions, n_elems).
+ *   d_elems       device, 16-byte aligned, n_elems elements of the create-time dtype;
+ *                 d_offsets[n_regions] <= n_elems is required (checked on device only
+ *                 with RS_FLAG_VALIDATE).  May be NULL when n_elems == 0.
+ *   n_regions     0 .. 2^31-1.
+ *   d_parent_ctx  device uint32[n_regions], the parent objects' context read by
+ *                 RS_OP_PARENT_LT nodes (indexed like the outputs); NULL when the
+ *                 pipeline has no such node (RS_ERR_INVALID_ARG if it has one).
+ *   out           device arrays of n_regions entries; they may be peer-mapped
+ *                 memory of another GPU (rs_ipc_open): the kernels then store the
+ *                 aggregates straight into that GPU's buffer over NVLink.
+ *   d_ws          workspace of >= rs_pipeline_workspace_bytes(p, n_regions, n_elems).
  * Asynchronous on `stream`. */
 rs_status rs_pipeline_run(rs_pipeline *p, const void *d_elems, int64_t n_elems,
-                          const int64_t *d_offsets, int64_t n_regions, rs_aggregates out,
-                          void *d_ws, size_t ws_bytes, rs_stream stream);
+                          const int64_t *d_offsets, int64_t n_regions, const void *d_parent_ctx,
+                          rs_aggregates out, void *d_ws, size_t ws_bytes, rs_stream stream);
 
 /* End-to-end convenience: same as rs_pipeline_run but with HOST buffers.
- * Copies elements and offsets host->device (pinned host memory gives
+ * Copies elements, offsets (and parent contexts) host->device (pinned host memory gives
  * asynchronous copies), runs, and copies the aggregates back into h_out;
  * device buffers are owned by the handle and grown on demand.  Synchronises
  * `stream` before returning. */
 rs_status rs_pipeline_run_host(rs_pipeline *p, const void *h_elems, int64_t n_elems,
-                               const int64_t *h_offsets, int64_t n_regions, rs_aggregates h_out,
-                               rs_stream stream);
+                               const int64_t *h_offsets, int64_t n_regions, const void *h_parent_ctx,
+                               rs_aggregates h_out, rs_stream stream);
 
 /* Copy the per-node counters of the last run into host_out[0..n_nodes-1]
  * (n_nodes = the create-time node count).  Synchronises `stream`. */
@@ -254,6 +265,49 @@ rs_status rs_pipeline_last_strategy(const rs_pipeline *p, int32_t *strategy);
 rs_status rs_pipeline_set_trace(rs_pipeline *p, void *d_trace, uint64_t bytes);
 
 void rs_pipeline_destroy(rs_pipeline *p);
+
+/* ------------------------------------------------------------- multi-GPU
+ * Regions are independent contexts (§1), so a stream partitioned by
+ * whole regions (rank k owns regions [base[k], base[k+1]), its run addressing
+ * them through d_offsets[base[k] .. base[k+1]]) needs no exchange while it is
+ * processed; the per-region aggregates are then assembled on one rank.
+ * NCCL is the library torch has loaded (found with dlopen; RS_NCCL_LIB may
+ * name another); the current CUDA device is the rank's GPU. */
+typedef struct rs_comm rs_comm;
+
+/* 128-byte NCCL unique id, created on one rank and passed to all (the caller
+ * distributes it, e.g. with torch.distributed). */
+rs_status rs_comm_unique_id(void *id128);
+
+/* Communicator of `world` ranks; this process is `rank`.  Collective. */
+rs_status rs_comm_init(const void *id128, int rank, int world, rs_comm **out);
+
+/* Gather: rank k's aggregates `local` (local_regions = region_base[k+1] -
+ * region_base[k] entries of the layout of aggregate op `agg_op`) are written to
+ * root_out.v*[region_base[k] ...] on rank `root`, at exact offsets (grouped
+ * ncclSend/ncclRecv, no padding; the root's own slice is a device copy).
+ * region_base: host int64[world+1], identical on all ranks.  root_out is read
+ * on the root only.  Stream-ordered on `stream`; collective. */
+rs_status rs_gather_aggregates(rs_comm *c, int32_t agg_op, rs_aggregates local, int64_t local_regions,
+                               const int64_t *region_base, rs_aggregates root_out, int root, rs_stream stream);
+
+/* Stream-ordered barrier (an all-reduce of one word): work enqueued on
+ * `stream` before it on every rank precedes work after it.  Collective. */
+rs_status rs_comm_barrier(rs_comm *c, rs_stream stream);
+
+void rs_comm_destroy(rs_comm *c);
+
+/* Peer-memory gather (fused with the aggregate's stores): the root exports
+ * its output buffer (64-byte CUDA IPC handle of the allocation holding d_buf,
+ * plus d_buf's byte offset in it; the caller passes both to the other ranks),
+ * the other ranks map the allocation and pass  mapped + offset + base[k] *
+ * bytes  as rs_aggregates to rs_pipeline_run, so the kernels store every
+ * region's aggregate into the root's buffer over NVLink as it completes.
+ * Completion: stream order + rs_comm_barrier (or a host barrier after a
+ * synchronise).  rs_ipc_open maps the allocation base; rs_ipc_close unmaps it. */
+rs_status rs_ipc_export(const void *d_buf, void *handle64, uint64_t *offset);
+rs_status rs_ipc_open(const void *handle64, void **d_ptr);
+rs_status rs_ipc_close(void *d_ptr);
 
 const char *rs_status_string(rs_status s);
 const char *rs_last_error(void);

@@ -39,7 +39,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 DTYPES = {"i32": 0, "u32": 1, "u8": 2, "f32": 3}
 NP_DTYPES = {"i32": np.int32, "u32": np.uint32, "u8": np.uint8, "f32": np.float32}
 FILTER, TRANSFORM = 2, 3
-OPS = {"hash_lt": (FILTER, 1), "lt_u32": (FILTER, 2), "class": (FILTER, 3),
+OPS = {"hash_lt": (FILTER, 1), "lt_u32": (FILTER, 2), "class": (FILTER, 3), "parent_lt": (FILTER, 4),
        "scale_f32": (TRANSFORM, 10), "affine_i32": (TRANSFORM, 11)}
 AGGS = {"sum_i64": 1, "sum_f32": 2, "count_min_u32": 3, "count_xor64": 4}
 STRATEGIES = {"signal": 0, "tagged": 1}
@@ -110,6 +110,7 @@ def lib():
 def _stages(spec):
     """Stage spec: list of tuples
     ("hash_lt", A, T) | ("lt_u32", bound) | ("class", 32-byte bitmap) |
+    ("parent_lt", uint32 ctx[R]: keep iff v < ctx[parent]) |
     ("scale_f32", float) | ("affine_i32", a, b)."""
     arr = (_Stage * max(1, len(spec)))()
     keep = []
@@ -125,6 +126,10 @@ def _stages(spec):
             buf = C.create_string_buffer(bytes(s[1]), 32)
             keep.append(buf)
             table = C.addressof(buf)
+        elif s[0] == "parent_lt":
+            ctx = np.ascontiguousarray(s[1], dtype=np.uint32)
+            keep.append(ctx)
+            table = ctx.ctypes.data
         elif s[0] == "scale_f32":
             p0 = struct.unpack("<I", struct.pack("<f", float(s[1])))[0]
         elif s[0] == "affine_i32":

@@ -41,7 +41,7 @@
  * names onto these numbers; nothing here is shared with include/rs.h.       */
 enum { OR_I32 = 0, OR_U32 = 1, OR_U8 = 2, OR_F32 = 3 };                /* element types   */
 enum { OR_FILTER = 2, OR_TRANSFORM = 3 };                               /* stage kinds     */
-enum { OR_HASH_LT = 1, OR_LT_U32 = 2, OR_CLASS = 3,                     /* filter ops (A13)*/
+enum { OR_HASH_LT = 1, OR_LT_U32 = 2, OR_CLASS = 3, OR_PARENT_LT = 4,   /* filter ops (A13)*/
        OR_SCALE_F32 = 10, OR_AFFINE_I32 = 11 };                         /* transform ops   */
 enum { OR_SUM_I64 = 1, OR_SUM_F32 = 2, OR_COUNT_MIN_U32 = 3, OR_COUNT_XOR64 = 4 };
 enum { OR_SIGNAL = 0, OR_TAGGED = 1 };                                  /* strategies      */
@@ -57,6 +57,7 @@ typedef struct {
                            /* LT_U32: p1 = bound; SCALE_F32: p0 = float bits    */
                            /* AFFINE_I32: p0 = a, p1 = b                        */
     const uint8_t *table;  /* CLASS: 32-byte bitmap over byte values            */
+                           /* PARENT_LT: uint32 parent context, one per region   */
 } or_stage;
 
 /* ------------------------------------------------------------- element ops */
@@ -73,8 +74,11 @@ static float bits_f(uint32_t b) { float f; memcpy(&f, &b, 4); return f; }
 static uint32_t f_bits(float f) { uint32_t b; memcpy(&b, &f, 4); return b; }
 
 /* isGood(v) of Fig. 5 is unspecified; readings in SURVEY §8(c) A13.
- * Returns 1 = keep.  Transforms always keep and rewrite *v (A14).           */
-static int apply_stage(const or_stage *s, uint32_t *v) {
+ * Returns 1 = keep.  Transforms always keep and rewrite *v (A14).
+ * r is the item's parent: a node "may access the parent object",
+ * Fig. 5 reads it with getParent(); PARENT_LT keeps an item iff
+ * it is below its parent's context value ctx[r] (reading R4).     */
+static int apply_stage(const or_stage *s, uint32_t *v, int64_t r) {
     if (s->kind == OR_FILTER) {
         switch (s->op) {
         case OR_HASH_LT: {                   /* keep iff top byte of v*A < T */
@@ -85,6 +89,8 @@ static int apply_stage(const or_stage *s, uint32_t *v) {
             return (uint64_t)*v < s->p1;
         case OR_CLASS:                       /* keep iff byte is in the set  */
             return (s->table[(*v & 0xFFu) >> 3] >> (*v & 7u)) & 1u;
+        case OR_PARENT_LT:                   /* keep iff v < parent context  */
+            return *v < ((const uint32_t *)s->table)[r];
         }
         return 1;
     }
@@ -144,7 +150,8 @@ static int check_args(int dtype, const void *elems, const int64_t *off, int64_t 
     if (agg < OR_SUM_I64 || agg > OR_COUNT_XOR64) return OR_EARG;
     for (int64_t r = 0; r < R; r++) if (off[r + 1] < off[r]) return OR_EARG;
     if (R > 0 && off[R] > off[0] && !elems) return OR_EARG;
-    for (int k = 0; k < nst; k++) if (st[k].op == OR_CLASS && !st[k].table) return OR_EARG;
+    for (int k = 0; k < nst; k++)
+        if ((st[k].op == OR_CLASS || st[k].op == OR_PARENT_LT) && !st[k].table) return OR_EARG;
     return OR_OK;
 }
 
@@ -165,7 +172,7 @@ int or_brute(int dtype, const void *elems, const int64_t *off, int64_t R,
         for (int64_t i = 0; i < n; i++) {
             uint32_t v = get_item(dtype, elems, off[r] + i);
             int keep = 1;
-            for (int k = 0; k < nst && keep; k++) keep = apply_stage(&st[k], &v);
+            for (int k = 0; k < nst && keep; k++) keep = apply_stage(&st[k], &v, r);
             if (keep) acc_run(agg, &a, v, i);
         }
         acc_end(agg, &a, out0, out1, r);
@@ -189,7 +196,7 @@ int or_node_counts(int dtype, const void *elems, const int64_t *off, int64_t R,
             uint32_t v = get_item(dtype, elems, g);
             int j = 0;
             row[0]++;
-            for (; j < nst; j++) { if (!apply_stage(&st[j], &v)) break; row[j + 1]++; }
+            for (; j < nst; j++) { if (!apply_stage(&st[j], &v, r)) break; row[j + 1]++; }
         }
     }
     return OR_OK;
@@ -501,7 +508,7 @@ static int run_ensemble(interp_t *I, int n, item_t *X, int64_t m) {
             }
             continue;
         }
-        if (apply_stage(&I->st[n - 1], &x.v)) emit_data(&I->e[n], x);   /* push */
+        if (apply_stage(&I->st[n - 1], &x.v, x.tag)) emit_data(&I->e[n], x);   /* push; tag = parent */
     }
     return OR_OK;
 }
@@ -656,6 +663,13 @@ int or_brute_range(int dtype, const void *elems, const int64_t *off, int64_t r0,
     if (r0 < 0 || r1 < r0) return OR_EARG;
     /* shift the output pointers so region r lands at index r */
     size_t s0 = (agg == OR_COUNT_MIN_U32) ? 4 : 8, s1 = (agg == OR_COUNT_MIN_U32) ? 4 : 8;
-    return or_brute(dtype, elems, off + r0, r1 - r0, st, nst, agg,
+    /* and the parent contexts, which are indexed by region like the outputs */
+    or_stage sh[16];
+    if (nst > 16) return OR_EARG;
+    for (int k = 0; k < nst; k++) {
+        sh[k] = st[k];
+        if (st[k].kind == OR_FILTER && st[k].op == OR_PARENT_LT) sh[k].table = (const uint8_t *)((const uint32_t *)st[k].table + r0);
+    }
+    return or_brute(dtype, elems, off + r0, r1 - r0, sh, nst, agg,
                     (char *)out0 + (size_t)r0 * s0, out1 ? (char *)out1 + (size_t)r0 * s1 : NULL);
 }

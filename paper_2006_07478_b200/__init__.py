@@ -18,9 +18,9 @@ LIB_PATH = os.environ.get("RS_LIB") or os.path.join(_HERE, "lib", "librs.so")
 
 # rs.h enumerations (kept in sync with include/rs.h by tests/test_abi.py)
 RS_OK, RS_ERR_INVALID_ARG, RS_ERR_INVALID_TOPOLOGY, RS_ERR_UNSUPPORTED = 0, -1, -2, -3
-RS_ERR_WORKSPACE, RS_ERR_CUDA, RS_ERR_PROTOCOL = -4, -5, -6
+RS_ERR_WORKSPACE, RS_ERR_CUDA, RS_ERR_PROTOCOL, RS_ERR_NCCL = -4, -5, -6, -7
 RS_NODE_ENUMERATE, RS_NODE_FILTER, RS_NODE_TRANSFORM, RS_NODE_AGGREGATE = 1, 2, 3, 4
-OPS = {"none": 0, "hash_lt": 1, "lt_u32": 2, "class": 3, "scale_f32": 10, "affine_i32": 11,
+OPS = {"none": 0, "hash_lt": 1, "lt_u32": 2, "class": 3, "parent_lt": 4, "scale_f32": 10, "affine_i32": 11,
        "sum_i64": 20, "sum_f32": 21, "count_min_u32": 22, "count_xor64": 23}
 DTYPES = {"i32": 0, "u32": 1, "u8": 2, "f32": 3}
 STRATEGIES = {"signal": 0, "tagged": 1, "auto": 2, "context": 3}
@@ -34,7 +34,8 @@ EXPORTS = ["rs_config_default", "rs_pipeline_create", "rs_pipeline_workspace_byt
            "rs_pipeline_kernel_times",
            "rs_pipeline_launches", "rs_pipeline_last_strategy",
            "rs_pipeline_geometry", "rs_pipeline_set_trace", "rs_pipeline_destroy", "rs_status_string",
-           "rs_last_error"]
+           "rs_last_error", "rs_comm_unique_id", "rs_comm_init", "rs_gather_aggregates", "rs_comm_barrier",
+           "rs_comm_destroy", "rs_ipc_export", "rs_ipc_open", "rs_ipc_close"]
 
 
 class RSError(RuntimeError):
@@ -77,8 +78,8 @@ def lib():
         L.rs_config_default.argtypes = [vp]
         L.rs_pipeline_create.argtypes = [vp, i32, i32, vp, C.POINTER(vp)]
         L.rs_pipeline_workspace_bytes.argtypes = [vp, i64, i64, C.POINTER(C.c_size_t)]
-        L.rs_pipeline_run.argtypes = [vp, vp, i64, vp, i64, rs_aggregates, vp, C.c_size_t, vp]
-        L.rs_pipeline_run_host.argtypes = [vp, vp, i64, vp, i64, rs_aggregates, vp]
+        L.rs_pipeline_run.argtypes = [vp, vp, i64, vp, i64, vp, rs_aggregates, vp, C.c_size_t, vp]
+        L.rs_pipeline_run_host.argtypes = [vp, vp, i64, vp, i64, vp, rs_aggregates, vp]
         L.rs_pipeline_stats.argtypes = [vp, vp, i32, vp]
         L.rs_pipeline_check.argtypes = [vp, vp, C.POINTER(C.c_int32)]
         L.rs_pipeline_profile.argtypes = [vp, vp, vp]
@@ -91,6 +92,18 @@ def lib():
         L.rs_pipeline_geometry.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         L.rs_pipeline_set_trace.argtypes = [vp, vp, C.c_uint64]
         L.rs_pipeline_set_trace.restype = i32
+        L.rs_comm_unique_id.argtypes = [vp]
+        L.rs_comm_init.argtypes = [vp, i32, i32, C.POINTER(vp)]
+        L.rs_gather_aggregates.argtypes = [vp, C.c_int32, rs_aggregates, i64, vp, rs_aggregates, i32, vp]
+        L.rs_comm_barrier.argtypes = [vp, vp]
+        L.rs_comm_destroy.argtypes = [vp]
+        L.rs_comm_destroy.restype = None
+        L.rs_ipc_export.argtypes = [vp, vp, C.POINTER(C.c_uint64)]
+        L.rs_ipc_open.argtypes = [vp, C.POINTER(vp)]
+        L.rs_ipc_close.argtypes = [vp]
+        for name in ("rs_comm_unique_id", "rs_comm_init", "rs_gather_aggregates", "rs_comm_barrier", "rs_ipc_export",
+                     "rs_ipc_open", "rs_ipc_close"):
+            getattr(L, name).restype = i32
         L.rs_pipeline_destroy.argtypes = [vp]
         L.rs_pipeline_destroy.restype = None
         L.rs_status_string.argtypes = [i32]
@@ -122,6 +135,8 @@ def _node(spec) -> tuple:
         return RS_NODE_FILTER, OPS[name], 0, int(spec[1]), None
     if name == "class":
         return RS_NODE_FILTER, OPS[name], 0, 0, bytes(spec[1])
+    if name == "parent_lt":                  # ("parent_lt",): contexts are passed to run(parent_ctx=...)
+        return RS_NODE_FILTER, OPS[name], 0, 0, None
     if name == "scale_f32":
         return RS_NODE_TRANSFORM, OPS[name], struct.unpack("<I", struct.pack("<f", float(spec[1])))[0], 0, None
     if name == "affine_i32":
@@ -212,9 +227,10 @@ class Pipeline:
         import torch
         return torch.empty(self.workspace_bytes(n_regions, n_elems) + 256, dtype=torch.uint8, device=device)
 
-    def run(self, elems, offsets, out, workspace, stream=None):
+    def run(self, elems, offsets, out, workspace, stream=None, parent_ctx=None):
         """elems: 1-D device tensor; offsets: int64 device tensor [R+1];
-        out: (v0, v1-or-None) device tensors; workspace: uint8 device tensor.
+        out: (v0, v1-or-None) device tensors; workspace: uint8 device tensor;
+        parent_ctx: uint32 (int32 view) device tensor [R] for PARENT_LT nodes.
         Asynchronous on `stream` (default: torch's current stream)."""
         import torch
         if stream is None:
@@ -224,14 +240,16 @@ class Pipeline:
         ws_bytes = workspace.numel() - (ws_ptr - workspace.data_ptr())
         agg = rs_aggregates(out[0].data_ptr(), out[1].data_ptr() if out[1] is not None else None)
         _check(lib().rs_pipeline_run(self.h, elems.data_ptr() if elems.numel() else None, elems.numel(),
-                                     offsets.data_ptr(), R, agg, ws_ptr, ws_bytes, C.c_void_p(stream.cuda_stream)))
+                                     offsets.data_ptr(), R, parent_ctx.data_ptr() if parent_ctx is not None else None,
+                                     agg, ws_ptr, ws_bytes, C.c_void_p(stream.cuda_stream)))
 
-    def run_raw(self, elems_ptr, n_elems, offsets_ptr, n_regions, out0_ptr, out1_ptr, ws_ptr, ws_bytes, stream_ptr):
+    def run_raw(self, elems_ptr, n_elems, offsets_ptr, n_regions, out0_ptr, out1_ptr, ws_ptr, ws_bytes, stream_ptr,
+                ctx_ptr=None):
         agg = rs_aggregates(out0_ptr, out1_ptr)
-        _check(lib().rs_pipeline_run(self.h, elems_ptr, n_elems, offsets_ptr, n_regions, agg, ws_ptr, ws_bytes,
-                                     C.c_void_p(stream_ptr)))
+        _check(lib().rs_pipeline_run(self.h, elems_ptr, n_elems, offsets_ptr, n_regions, ctx_ptr, agg, ws_ptr,
+                                     ws_bytes, C.c_void_p(stream_ptr)))
 
-    def run_host(self, elems, offsets, out0, out1=None, stream=None):
+    def run_host(self, elems, offsets, out0, out1=None, stream=None, parent_ctx=None):
         """Host (numpy or pinned CPU tensor) in, host out; synchronous."""
         import torch
 
@@ -243,7 +261,8 @@ class Pipeline:
         R = (offsets.numel() if isinstance(offsets, torch.Tensor) else offsets.size) - 1
         s = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
         agg = rs_aggregates(ptr(out0), ptr(out1))
-        _check(lib().rs_pipeline_run_host(self.h, ptr(elems) if n else None, n, ptr(offsets), R, agg, C.c_void_p(s)))
+        _check(lib().rs_pipeline_run_host(self.h, ptr(elems) if n else None, n, ptr(offsets), R, ptr(parent_ctx), agg,
+                                          C.c_void_p(s)))
 
     def stats(self, stream=None):
         import numpy as np
@@ -300,3 +319,60 @@ class Pipeline:
         g, w, c = C.c_int32(), C.c_int32(), C.c_int32()
         _check(lib().rs_pipeline_geometry(self.h, C.byref(g), C.byref(w), C.byref(c)))
         return {"grid": g.value, "warps_per_cta": w.value, "chunk": c.value}
+
+
+# ------------------------------------------------------------- multi-GPU (rs.h)
+class Comm:
+    """rs_comm handle: NCCL communicator of the C ABI (the aggregate gather)."""
+
+    def __init__(self, uid: bytes, rank: int, world: int):
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(uid), 128)
+        _check(lib().rs_comm_init(buf, rank, world, C.byref(h)))
+        self.h, self.rank, self.world = h, rank, world
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().rs_comm_unique_id(buf))
+        return buf.raw
+
+    def gather(self, agg, local, bounds, root_out, root=0, stream=None):
+        """rs_gather_aggregates: local = (v0, v1-or-None) device tensors of this
+        rank's regions; bounds = world+1 region bases; root_out read on `root`."""
+        import torch
+        s = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        base = (C.c_int64 * len(bounds))(*[int(b) for b in bounds])
+        loc = rs_aggregates(local[0].data_ptr(), local[1].data_ptr() if local[1] is not None else None)
+        ro = rs_aggregates(root_out[0].data_ptr() if root_out is not None else None,
+                           root_out[1].data_ptr() if root_out is not None and root_out[1] is not None else None)
+        n = int(bounds[self.rank + 1] - bounds[self.rank])
+        _check(lib().rs_gather_aggregates(self.h, OPS[agg], loc, n, base, ro, root, C.c_void_p(s)))
+
+    def barrier(self, stream=None):
+        import torch
+        s = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _check(lib().rs_comm_barrier(self.h, C.c_void_p(s)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().rs_comm_destroy(self.h)
+            self.h = None
+
+
+def ipc_export(ptr: int):
+    """(64-byte handle of the allocation holding ptr, ptr's offset in it)."""
+    buf = C.create_string_buffer(64)
+    off = C.c_uint64()
+    _check(lib().rs_ipc_export(C.c_void_p(ptr), buf, C.byref(off)))
+    return buf.raw, int(off.value)
+
+
+def ipc_open(handle: bytes) -> int:
+    p = C.c_void_p()
+    _check(lib().rs_ipc_open(C.create_string_buffer(bytes(handle), 64), C.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr: int):
+    _check(lib().rs_ipc_close(C.c_void_p(ptr)))

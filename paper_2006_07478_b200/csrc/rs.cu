@@ -28,6 +28,8 @@ bool is_pow2(uint32_t x) { return x && !(x & (x - 1)); }
 
 }  // namespace
 
+void rsk::set_last_error(const std::string &m) { g_err = m; }
+
 struct rs_pipeline {
     rs_config cfg;
     rs_dtype elem;
@@ -49,6 +51,7 @@ struct rs_pipeline {
     rs_pipeline *sub[2] = {nullptr, nullptr};
     uint32_t auto_min_len = 0;
     cudaStream_t last_stream = nullptr;
+    bool has_parent = false;      // a PARENT_LT node reads d_parent_ctx
     // RS_FLAG_TRACE event buffer (caller-owned device memory)
     void *trace = nullptr;
     uint64_t trace_bytes = 0;
@@ -133,6 +136,7 @@ const char *rs_status_string(rs_status s) {
         case RS_ERR_WORKSPACE: return "RS_ERR_WORKSPACE";
         case RS_ERR_CUDA: return "RS_ERR_CUDA";
         case RS_ERR_PROTOCOL: return "RS_ERR_PROTOCOL";
+        case RS_ERR_NCCL: return "RS_ERR_NCCL";
     }
     return "RS_ERR_UNKNOWN";
 }
@@ -183,6 +187,10 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     }
     if (cfg.strategy == RS_STRATEGY_AUTO && (cfg.flags & RS_FLAG_TRACE))
         return fail(RS_ERR_UNSUPPORTED, "RS_FLAG_TRACE is built for SUM_I64 pipelines under the signal strategy");
+    if (cfg.strategy == RS_STRATEGY_AUTO)
+        for (int i = 1; i < n_nodes - 1; ++i)
+            if (nodes[i].kind == RS_NODE_FILTER && nodes[i].op == RS_OP_PARENT_LT)
+                return fail(RS_ERR_UNSUPPORTED, "PARENT_LT is built for the signal strategy (uniform context per ensemble, P:464-465)");
     if (cfg.strategy == RS_STRATEGY_AUTO) {
         rs_config c = cfg;
         rs_pipeline *a = nullptr, *b = nullptr;
@@ -264,6 +272,14 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
                     if (nd.p1 > (1ull << 32)) { delete p; return fail(RS_ERR_INVALID_ARG, "LT_U32 bound must be <= 2^32"); }
                     s.b = (uint32_t)nd.p1;
                     s.table[0] = nd.p1 == (1ull << 32);
+                    break;
+                case RS_OP_PARENT_LT:
+                    if (elem == RS_U8) { delete p; return fail(RS_ERR_UNSUPPORTED, "PARENT_LT needs 4-byte elements"); }
+                    if (cfg.strategy != RS_STRATEGY_SIGNAL) {
+                        delete p;
+                        return fail(RS_ERR_UNSUPPORTED, "PARENT_LT is built for the signal strategy (uniform context per ensemble, P:464-465)");
+                    }
+                    p->has_parent = true;
                     break;
                 case RS_OP_CLASS:
                     if (!nd.table) { delete p; return fail(RS_ERR_INVALID_ARG, "CLASS needs a 32-byte table"); }
@@ -372,7 +388,8 @@ static rs_status prepare(rs_pipeline *p, const void *d_elems, int64_t n_elems, c
 }
 
 static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, const int64_t *d_offsets,
-                          int64_t n_regions, rs_aggregates out, void *d_ws, size_t ws_bytes, cudaStream_t stream) {
+                          int64_t n_regions, const void *d_ctx, rs_aggregates out, void *d_ws, size_t ws_bytes,
+                          cudaStream_t stream) {
     if (!p) return fail(RS_ERR_INVALID_ARG, "pipeline is NULL");
     p->launches = 0;
     if (n_regions < 0 || n_regions >= (1ll << 31)) return fail(RS_ERR_INVALID_ARG, "n_regions must be in [0, 2^31)");
@@ -396,6 +413,10 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
         pa.K.auto_sel = 1;
         pb.K.auto_sel = 2;
     }
+    if (p->has_parent && !d_ctx) return fail(RS_ERR_INVALID_ARG, "a PARENT_LT node needs d_parent_ctx");
+    if (d_ctx && ((uintptr_t)d_ctx & 3u)) return fail(RS_ERR_INVALID_ARG, "d_parent_ctx must be 4-byte aligned");
+    pa.K.ctx = (const uint32_t *)d_ctx;
+    pb.K.ctx = (const uint32_t *)d_ctx;
     KParams Kpre = pa.K;
     if (is_auto) {
         Kpre.tagged = -1;
@@ -433,13 +454,14 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
 }
 
 rs_status rs_pipeline_run(rs_pipeline *p, const void *d_elems, int64_t n_elems, const int64_t *d_offsets,
-                          int64_t n_regions, rs_aggregates out, void *d_ws, size_t ws_bytes, rs_stream stream) {
+                          int64_t n_regions, const void *d_parent_ctx, rs_aggregates out, void *d_ws, size_t ws_bytes,
+                          rs_stream stream) {
     if (!p) return fail(RS_ERR_INVALID_ARG, "pipeline is NULL");
-    return run_impl(p, d_elems, n_elems, d_offsets, n_regions, out, d_ws, ws_bytes, (cudaStream_t)stream);
+    return run_impl(p, d_elems, n_elems, d_offsets, n_regions, d_parent_ctx, out, d_ws, ws_bytes, (cudaStream_t)stream);
 }
 
 rs_status rs_pipeline_run_host(rs_pipeline *p, const void *h_elems, int64_t n_elems, const int64_t *h_offsets,
-                               int64_t n_regions, rs_aggregates h_out, rs_stream stream_) {
+                               int64_t n_regions, const void *h_parent_ctx, rs_aggregates h_out, rs_stream stream_) {
     if (!p) return fail(RS_ERR_INVALID_ARG, "pipeline is NULL");
     if (n_regions < 0 || n_elems < 0) return fail(RS_ERR_INVALID_ARG, "negative size");
     if (n_regions == 0) return RS_OK;
@@ -455,7 +477,8 @@ rs_status rs_pipeline_run_host(rs_pipeline *p, const void *h_elems, int64_t n_el
     const size_t b_off = align256(8 * (size_t)(n_regions + 1));
     const size_t b_o0 = align256((size_t)L.out_bytes0 * (size_t)n_regions);
     const size_t b_o1 = align256((size_t)(L.out_bytes1 ? L.out_bytes1 : 1) * (size_t)n_regions);
-    const size_t need = b_el + b_off + b_o0 + b_o1 + ws;
+    const size_t b_ctx = h_parent_ctx ? align256(4 * (size_t)n_regions) : 0;
+    const size_t need = b_el + b_off + b_o0 + b_o1 + b_ctx + ws;
     if (p->h_dbuf_bytes < need) {
         if (p->h_dbuf) cudaFree(p->h_dbuf);
         p->h_dbuf = nullptr;
@@ -465,13 +488,16 @@ rs_status rs_pipeline_run_host(rs_pipeline *p, const void *h_elems, int64_t n_el
     }
     uint8_t *d = (uint8_t *)p->h_dbuf;
     void *d_el = d, *d_off = d + b_el, *d_o0 = d + b_el + b_off, *d_o1 = d + b_el + b_off + b_o0;
-    void *d_ws = d + b_el + b_off + b_o0 + b_o1;
+    void *d_ctx = h_parent_ctx ? d + b_el + b_off + b_o0 + b_o1 : nullptr;
+    void *d_ws = d + b_el + b_off + b_o0 + b_o1 + b_ctx;
     if (n_elems && cudaMemcpyAsync(d_el, h_elems, esz * (size_t)n_elems, cudaMemcpyHostToDevice, stream) != cudaSuccess)
         return fail(RS_ERR_CUDA, "H2D elements failed");
     if (cudaMemcpyAsync(d_off, h_offsets, 8 * (size_t)(n_regions + 1), cudaMemcpyHostToDevice, stream) != cudaSuccess)
         return fail(RS_ERR_CUDA, "H2D offsets failed");
+    if (d_ctx && cudaMemcpyAsync(d_ctx, h_parent_ctx, 4 * (size_t)n_regions, cudaMemcpyHostToDevice, stream) != cudaSuccess)
+        return fail(RS_ERR_CUDA, "H2D parent contexts failed");
     rs_aggregates dout{d_o0, L.out_bytes1 ? d_o1 : nullptr};
-    rs_status s = run_impl(p, d_el, n_elems, (const int64_t *)d_off, n_regions, dout, d_ws, ws, stream);
+    rs_status s = run_impl(p, d_el, n_elems, (const int64_t *)d_off, n_regions, d_ctx, dout, d_ws, ws, stream);
     if (s != RS_OK) return s;
     if (cudaMemcpyAsync(h_out.v0, d_o0, (size_t)L.out_bytes0 * (size_t)n_regions, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
         return fail(RS_ERR_CUDA, "D2H aggregates failed");

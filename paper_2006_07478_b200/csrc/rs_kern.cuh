@@ -30,6 +30,8 @@
 
 #include <cuda_runtime.h>
 
+#include <string>
+
 using namespace rs;
 
 namespace rsk {
@@ -87,6 +89,7 @@ struct KParams {
     uint32_t auto_min_len;          // AUTO: signal iff children >= auto_min_len * regions
     int32_t nst;
     StageP st[MAXK];
+    const uint32_t *ctx;            // parent context, one uint32 per region (PARENT_LT), or null
     uint32_t *trace;                // RS_FLAG_TRACE: [0] events written, events of 8 words from word 8
     uint32_t trace_cap;             // events the buffer holds
 };
@@ -98,6 +101,7 @@ __device__ __forceinline__ bool stage_apply(const StageP &s, uint32_t &v) {
         case RS_OP_HASH_LT: return ((v * s.a) >> 24) < s.b;
         case RS_OP_LT_U32: return s.table[0] ? true : v < s.b;    // table[0]: bound == 2^32
         case RS_OP_CLASS: return (s.table[(v & 0xffu) >> 5] >> (v & 31u)) & 1u;
+        case RS_OP_PARENT_LT: return true;     // signal strategy only: applied through OpLt (rs_pipe.cuh)
         case RS_OP_SCALE_F32: v = __float_as_uint(__fmul_rn(__uint_as_float(s.a), __uint_as_float(v))); return true;
         case RS_OP_AFFINE_I32: v = v * s.a + s.b; return true;
     }
@@ -205,6 +209,9 @@ struct Launch {
     uint32_t ring0;                 // Q0 ring capacity (elements) of the sequential kernel
     int out_bytes0, out_bytes1;
 };
+
+// rs_last_error()'s thread-local message (rs.cu), shared by the other host units.
+void set_last_error(const std::string &m);
 
 // One per aggregate, defined in rs_k<AGG>.cu.
 Launch launch_agg20(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);

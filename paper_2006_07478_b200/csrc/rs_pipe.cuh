@@ -156,8 +156,9 @@ __device__ __noinline__ uint32_t partial_stage(const Op op, const uint32_t *in, 
 // Calls f(op) with the node's op as its specialised functor (one switch per
 // firing instead of one per item).
 template <class F>
-__device__ __forceinline__ void with_op(const StageP &sp, F &&f) {
+__device__ __forceinline__ void with_op(const StageP &sp, uint32_t pv, F &&f) {
     switch (sp.op) {
+        case RS_OP_PARENT_LT: f(OpLt{pv, false}); break;   // pv = the open region's context (getParent)
         case RS_OP_HASH_LT:
             if (sp.b >= 256) f(OpAll{});
             else f(OpHash{sp.a, sp.b << 24});
@@ -346,8 +347,9 @@ struct Pipe {
     // per-instance shared header: [0,64) TMA barriers, [64,160) node counters
     // (u32 x 24: data firings, full firings, items, signals per node),
     // [160,288) RS_FLAG_PROFILE cycle counters (u64 x 16)
-    static constexpr uint32_t HDR = CTX ? 416 : 288;     // CTX: + 32-word key scratch at [288, 416)
-    static constexpr uint32_t CNT_OFF = 64, PROF_OFF = 160, SCR_OFF = 288;
+    // [288, 320) parent-context value of the open region per node (PARENT_LT)
+    static constexpr uint32_t HDR = CTX ? 448 : 320;     // CTX: + 32-word key scratch at [320, 448)
+    static constexpr uint32_t CNT_OFF = 64, PROF_OFF = 160, PV_OFF = 288, SCR_OFF = 320;
 
     const KParams &P;
     const int lane;
@@ -607,6 +609,22 @@ struct Pipe {
             else { pe = e; key = r; }
         }
     }
+
+    // getParent() (Fig. 5) for PARENT_LT nodes: under the
+    // signal strategy every ensemble lies in the open region (P:464-465,
+    // P:495-499), so a node loads its region's context once, on Begin, and
+    // the filter compares each item with that one value.
+    __device__ __forceinline__ uint32_t region_key(uint32_t key) const {
+        if (!(key & SLOT)) return key;
+        const uint32_t slot = key & ~SLOT, k = slot >> 1;
+        return ((slot & 1u) ? P.chunk_fr[k + 1] : P.chunk_fr[k]) - 1u;
+    }
+    __device__ __forceinline__ void set_pv(int n, uint32_t key) const {
+        const uint32_t v = P.ctx[region_key(key)];
+        if (lane == 0) reinterpret_cast<uint32_t *>(base + PV_OFF)[n] = v;
+        __syncwarp();
+    }
+    __device__ __forceinline__ uint32_t pvn(int n) const { return reinterpret_cast<const uint32_t *>(base + PV_OFF)[n]; }
 
     // Sender rule for one signal on edge e: S empty -> |Q|;
     // otherwise items emitted since the tail signal.  Resets the counter.
@@ -967,6 +985,7 @@ struct Pipe {
                     else fused_run(in, tin, imask, h, nens, OpLt{sp.b, false});
                     break;
                 case RS_OP_CLASS: fused_run(in, tin, imask, h, nens, OpClass{sp.table}); break;
+                case RS_OP_PARENT_LT: fused_run(in, tin, imask, h, nens, OpLt{pvn(n), false}); break;
                 case RS_OP_SCALE_F32: fused_run(in, tin, imask, h, nens, OpScale{__uint_as_float(sp.a)}); break;
                 default: fused_run(in, tin, imask, h, nens, OpAffine{sp.a, sp.b}); break;
             }
@@ -982,6 +1001,7 @@ struct Pipe {
                     else filter_full<n>(in, tin, imask, h, nens, OpLt{sp.b, false});
                     break;
                 case RS_OP_CLASS: filter_full<n>(in, tin, imask, h, nens, OpClass{sp.table}); break;
+                case RS_OP_PARENT_LT: filter_full<n>(in, tin, imask, h, nens, OpLt{pvn(n), false}); break;
                 case RS_OP_SCALE_F32: filter_full<n>(in, tin, imask, h, nens, OpScale{__uint_as_float(sp.a)}); break;
                 default: filter_full<n>(in, tin, imask, h, nens, OpAffine{sp.a, sp.b}); break;
             }
@@ -1061,6 +1081,9 @@ struct Pipe {
                 ++nsig;
                 const bool is_end = (hs.y & END_BIT) != 0;
                 if constexpr (TR) trace_event(n, is_end ? TR_END : TR_BEGIN, hs.x, 0u, 0u, 0u);
+                if constexpr (n <= K) {
+                    if (!is_end && P.st[n - 1].op == RS_OP_PARENT_LT) set_pv(n, hs.x);
+                }
                 if constexpr (AGGN) {
                     if (!is_end) {               // a::begin: acc = identity
                         acc = AT::id();
@@ -1098,11 +1121,6 @@ struct Pipe {
     // P:375-379) and that the items per bracket equal the oracle's count
     // (Lemma 1).  Only the trace instantiations contain this code.
     uint32_t tseq = 0;
-    __device__ __forceinline__ uint32_t region_of(uint32_t key) const {
-        if (!(key & SLOT)) return key;
-        const uint32_t slot = key & ~SLOT, k = slot >> 1;
-        return ((slot & 1u) ? P.chunk_fr[k + 1] : P.chunk_fr[k]) - 1u;
-    }
     __device__ __forceinline__ void trace_event(uint32_t n, uint32_t type, uint32_t key, uint32_t cnt, uint32_t lo,
                                              uint32_t hi) {
         if (lane == 0) {
@@ -1113,7 +1131,7 @@ struct Pipe {
                 e[1] = tseq;
                 e[2] = n | (type << 8);
                 e[3] = key;
-                e[4] = type == TR_ENSEMBLE ? 0u : region_of(key);
+                e[4] = type == TR_ENSEMBLE ? 0u : region_key(key);
                 e[5] = cnt;
                 e[6] = lo;
                 e[7] = hi;
@@ -1204,9 +1222,9 @@ struct Pipe {
             uint32_t done = e;
             if constexpr (AGGN) {
                 if constexpr (n == K + 1) ctx_agg_ens(in, imask, E<ei>().qh, e, cons, OpAll{});
-                else with_op(P.st[n - 1], [&](auto op) { ctx_agg_ens(in, imask, E<ei>().qh, e, cons, op); });
+                else with_op(P.st[n - 1], 0u, [&](auto op) { ctx_agg_ens(in, imask, E<ei>().qh, e, cons, op); });
             } else {
-                with_op(P.st[n - 1], [&](auto op) { done = ctx_filter_ens<n>(in, imask, E<ei>().qh, e, cons, op); });
+                with_op(P.st[n - 1], 0u, [&](auto op) { done = ctx_filter_ens<n>(in, imask, E<ei>().qh, e, cons, op); });
             }
             if (done == 0) break;
             E<ei>().qh += done;
@@ -1436,7 +1454,7 @@ struct Pipe {
             }
         } else if constexpr (NA && n == K) {
             if constexpr (!TAG) {
-                with_op(P.st[n - 1], [&](auto op) {
+                with_op(P.st[n - 1], pvn(n), [&](auto op) {
                     const FusedAcc<AT> r = fused_partial<AT, decltype(op), AGG_U8IN>(in, imask, h, e, op, adelta, P.C - 1,
                                                                                      FusedAcc<AT>{acc, fkept});
                     acc = r.acc;
@@ -1447,7 +1465,7 @@ struct Pipe {
             }
         } else {
             uint32_t tl = E<n>().qt;
-            with_op(P.st[n - 1], [&](auto op) {
+            with_op(P.st[n - 1], pvn(n), [&](auto op) {
                 tl = partial_stage<TAG, decltype(op), U8 && n == 1>(op, in, tin, imask, h, e, Q<n>(), T<n>(), qm<n>(),
                                                                     tl, lt, P.C - 1);
             });

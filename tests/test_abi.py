@@ -94,16 +94,16 @@ def test_run_argument_errors_before_launch(rs):
     L = rs.lib()
     agg = rs.rs_aggregates(0x1000, None)
     # negative region count
-    assert L.rs_pipeline_run(p.h, 0x1000, 10, 0x1000, -1, agg, 0x1000, ws, None) == rs.RS_ERR_INVALID_ARG
+    assert L.rs_pipeline_run(p.h, 0x1000, 10, 0x1000, -1, None, agg, 0x1000, ws, None) == rs.RS_ERR_INVALID_ARG
     # R = 0 is a no-op
-    assert L.rs_pipeline_run(p.h, None, 0, 0x1000, 0, agg, None, 0, None) == rs.RS_OK
+    assert L.rs_pipeline_run(p.h, None, 0, 0x1000, 0, None, agg, None, 0, None) == rs.RS_OK
     # misaligned elements
-    assert L.rs_pipeline_run(p.h, 0x1004, 10, 0x1000, 1, agg, 0x1000, ws, None) == rs.RS_ERR_INVALID_ARG
+    assert L.rs_pipeline_run(p.h, 0x1004, 10, 0x1000, 1, None, agg, 0x1000, ws, None) == rs.RS_ERR_INVALID_ARG
     # workspace too small
-    assert L.rs_pipeline_run(p.h, 0x1000, 10, 0x1000, 1, agg, 0x1000, 16, None) == rs.RS_ERR_WORKSPACE
+    assert L.rs_pipeline_run(p.h, 0x1000, 10, 0x1000, 1, None, agg, 0x1000, 16, None) == rs.RS_ERR_WORKSPACE
     # null output
     bad = rs.rs_aggregates(None, None)
-    assert L.rs_pipeline_run(p.h, 0x1000, 10, 0x1000, 1, bad, 0x1000, ws, None) == rs.RS_ERR_INVALID_ARG
+    assert L.rs_pipeline_run(p.h, 0x1000, 10, 0x1000, 1, None, bad, 0x1000, ws, None) == rs.RS_ERR_INVALID_ARG
     assert "NULL" in L.rs_last_error().decode()
 
 

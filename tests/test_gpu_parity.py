@@ -384,3 +384,83 @@ def test_context_empty_region_runs(rs, thr, L):
             kc = oracle.node_counts(v, off, st)
             for j in range(len(st) + 1):
                 assert stt[j + 1][2] == kc[:, j].sum()
+
+
+def test_comm_world1_gather_and_barrier(rs):
+    """The C ABI's NCCL gather at world size 1 (the box has one GPU): the root's
+    own slice is placed at its region base; barrier and destroy work."""
+    uid = rs.Comm.unique_id()
+    c = rs.Comm(uid, 0, 1)
+    try:
+        loc = (torch.arange(100, dtype=torch.int64, device="cuda") * 3, None)
+        root = (torch.full((100,), -1, dtype=torch.int64, device="cuda"), None)
+        c.gather("sum_i64", loc, [0, 100], root, root=0)
+        c.barrier()
+        torch.cuda.synchronize()
+        assert torch.equal(root[0], loc[0])
+        cnt = (torch.arange(7, dtype=torch.int32, device="cuda"), torch.arange(7, 14, dtype=torch.int32, device="cuda"))
+        rc = (torch.zeros(7, dtype=torch.int32, device="cuda"), torch.zeros(7, dtype=torch.int32, device="cuda"))
+        c.gather("count_min_u32", cnt, [0, 7], rc, root=0)
+        torch.cuda.synchronize()
+        assert torch.equal(rc[0], cnt[0]) and torch.equal(rc[1], cnt[1])
+        with pytest.raises(rs.RSError):           # local size does not match the partition
+            c.gather("sum_i64", loc, [0, 50], root, root=0)
+    finally:
+        c.close()
+
+
+def test_ipc_export_offset(rs):
+    """rs_ipc_export reports the buffer's offset inside its allocation (the
+    caching allocator hands out sub-ranges), so a peer maps base + offset."""
+    big = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    sub = big[4096:]
+    h, off = rs.ipc_export(sub.data_ptr())
+    assert len(h) == 64 and off >= 4096 and (off - 4096) == rs.ipc_export(big.data_ptr())[1]
+
+
+def test_parent_context_signal(rs):
+    """PARENT_LT (getParent, Fig. 5): each item is kept iff
+    it is below its region's context value -- bit-exact against the oracle, with
+    regions split across chunks (the context of a split region is loaded by
+    every part) and empty regions."""
+    g = np.random.default_rng(5)
+    lens = synth.lengths(3000, "zipf", seed=9, zipf_max=6000)
+    lens[::11] = 0
+    off = synth.offsets(lens, base=3)
+    vals = synth.values(int(off[-1]) + 2, "i32", seed=10)
+    ctx = g.integers(0, 2**32, off.size - 1, dtype=np.uint64).astype(np.uint32)
+    for stages in ([("parent_lt", ctx)], [("hash_lt", 0x9E3779B1, 192), ("parent_lt", ctx)],
+                   [("parent_lt", ctx), ("hash_lt", 0x85EBCA6B, 192), ("parent_lt", ctx)]):
+        ref = oracle.brute(vals, off, stages, "sum_i64")
+        dev_stages = [s if s[0] != "parent_lt" else ("parent_lt",) for s in stages]
+        for mode in ("seq", "unfused"):
+            flags = rs.RS_FLAG_STATS | (rs.RS_FLAG_UNFUSED if mode == "unfused" else 0)
+            p = rs.Pipeline(dev_stages, "sum_i64", strategy="signal", flags=flags, chunk=2048)
+            e = torch.from_numpy(vals).cuda()
+            o = torch.from_numpy(off).cuda()
+            cx = torch.from_numpy(ctx.view(np.int32)).cuda()
+            R = off.size - 1
+            out = p.alloc_outputs(R)
+            ws = p.alloc_workspace(R, e.numel())
+            p.run(e, o, out, ws, parent_ctx=cx)
+            torch.cuda.synchronize()
+            assert p.check() == 0
+            np.testing.assert_array_equal(out[0].cpu().numpy(), ref[0])
+            with pytest.raises(rs.RSError):       # the context array is required
+                p.run(e, o, out, ws)
+    with pytest.raises(rs.RSError) as ex:
+        rs.Pipeline([("parent_lt",)], "sum_i64", strategy="tagged")
+    assert ex.value.status == rs.RS_ERR_UNSUPPORTED
+
+
+def test_auto_decides_on_call_children(rs):
+    """AUTO decides from the call's own children count off[R] - off[0], not
+    from the array bound (a one-region batch over a large array runs the
+    strategy its own length calls for)."""
+    lens = synth.lengths(4000, "fixed", L=16)
+    off = synth.offsets(lens)
+    vals = synth.values(int(off[-1]) + (1 << 22), "i32", seed=4)      # array far longer than the regions
+    stages = synth.sweep_stages(3)
+    got, _, p = run_gpu(rs, vals, off, stages, "sum_i64", "auto")
+    assert p.last_strategy() == "tagged"
+    assert_parity(got, oracle.brute(vals, off, stages, "sum_i64"), "sum_i64")

@@ -404,3 +404,32 @@ def test_brute_sharded_prefix_identity(threads):
     ref_mn = np.full(off.size - 1, 0xFFFFFFFF, np.uint64)
     np.minimum.at(ref_mn, reg, u[off[0]:].astype(np.uint64))
     np.testing.assert_array_equal(mn.astype(np.uint64), ref_mn)
+
+
+# ------------------------------------------------- parent context (getParent)
+def test_parent_lt_by_construction():
+    """PARENT_LT keeps item v of parent r iff (uint32)v < ctx[r] (a node reads
+    its parent object; Fig. 5 getParent).  ctx[r] is set
+    to one more than the k_r-th smallest value of region r, so exactly the k_r
+    smallest survive; their sum comes from numpy's sort, not the oracle."""
+    g = np.random.default_rng(3)
+    lens = synth.lengths(400, "uniform", lo=0, hi=60, seed=4)
+    off = synth.offsets(lens, base=5)
+    n = int(off[-1])
+    vals = g.permutation(np.arange(1, n + 1, dtype=np.int64) * 7).astype(np.uint32).view(np.int32)   # distinct, < 2^31
+    ctx = np.zeros(off.size - 1, np.uint32)
+    expect = np.zeros(off.size - 1, np.int64)
+    u = vals.view(np.uint32)
+    for r in range(off.size - 1):
+        seg = np.sort(u[off[r]:off[r + 1]].astype(np.int64))
+        k = int(g.integers(0, seg.size + 1))
+        ctx[r] = (seg[k - 1] + 1) if k > 0 else 0
+        expect[r] = seg[:k].sum()
+    stages = [("parent_lt", ctx)]
+    np.testing.assert_array_equal(oracle.brute(vals, off, stages, "sum_i64")[0], expect)
+    for strat in ("signal", "tagged"):
+        np.testing.assert_array_equal(oracle.interp(vals, off, stages, "sum_i64", strategy=strat)["out"][0], expect)
+    np.testing.assert_array_equal(oracle.brute_sharded(vals, off, stages, "sum_i64", threads=5)[0], expect)
+    # node counts: survivors of region r at the aggregate = k_r
+    kc = oracle.node_counts(vals, off, stages)
+    np.testing.assert_array_equal(kc[:, 1], [np.count_nonzero(u[off[r]:off[r + 1]] < ctx[r]) for r in range(off.size - 1)])
