@@ -403,8 +403,13 @@ def test_comm_world1_gather_and_barrier(rs):
         c.gather("count_min_u32", cnt, [0, 7], rc, root=0)
         torch.cuda.synchronize()
         assert torch.equal(rc[0], cnt[0]) and torch.equal(rc[1], cnt[1])
-        with pytest.raises(rs.RSError):           # local size does not match the partition
-            c.gather("sum_i64", loc, [0, 50], root, root=0)
+        # local_regions that disagrees with region_base is rejected before any NCCL call
+        import ctypes as C
+        base = (C.c_int64 * 2)(0, 50)
+        agg = rs.rs_aggregates(loc[0].data_ptr(), None)
+        st = rs.lib().rs_gather_aggregates(c.h, rs.OPS["sum_i64"], agg, 100, base,
+                                           rs.rs_aggregates(root[0].data_ptr(), None), 0, None)
+        assert st == rs.RS_ERR_INVALID_ARG
     finally:
         c.close()
 
