@@ -115,7 +115,8 @@ enum {
     RS_FLAG_STATS = 1u,      /* collect per-node occupancy counters (default on)     */
     RS_FLAG_VALIDATE = 2u,   /* device-check offsets monotone and <= n_elems          */
     RS_FLAG_TIMING = 4u,     /* record CUDA events around each kernel of a run        */
-    RS_FLAG_PROFILE = 16u,   /* per-node clock64() cycle counters (rs_pipeline_profile)  */
+    RS_FLAG_PROFILE = 16u,   /* per-node clock64() cycle counters (rs_pipeline_profile); like
+                                RS_FLAG_TRACE a debug instantiation (SUM_I64, signal strategy) */
     RS_FLAG_RESERVED8 = 8u,  /* round 1's warp-specialised scheduler (removed: slower than the
                                 sequential one); create rejects it with RS_ERR_UNSUPPORTED */
     RS_FLAG_TRACE = 64u,     /* §8(c) trace mode (SUM_I64, signal strategy only; needs

@@ -88,7 +88,7 @@ uint32_t auto_default(int nst) {
 }
 
 bool get_launch(const rs_pipeline *p, Launch *L) {
-    if (p->cfg.flags & RS_FLAG_TRACE) {
+    if (p->cfg.flags & (RS_FLAG_TRACE | RS_FLAG_PROFILE)) {    // the debug instantiations
         *L = launch_agg20_trace(p->nst, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap,
                                 p->cfg.q0_stage);
         return true;
@@ -185,7 +185,7 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
             break;
         default: return fail(RS_ERR_UNSUPPORTED, "unknown aggregate op");
     }
-    if (cfg.strategy == RS_STRATEGY_AUTO && (cfg.flags & RS_FLAG_TRACE))
+    if (cfg.strategy == RS_STRATEGY_AUTO && (cfg.flags & (RS_FLAG_TRACE | RS_FLAG_PROFILE)))
         return fail(RS_ERR_UNSUPPORTED, "RS_FLAG_TRACE is built for SUM_I64 pipelines under the signal strategy");
     if (cfg.strategy == RS_STRATEGY_AUTO)
         for (int i = 1; i < n_nodes - 1; ++i)
@@ -216,8 +216,8 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     }
     if (cfg.strategy != RS_STRATEGY_SIGNAL && cfg.strategy != RS_STRATEGY_TAGGED && cfg.strategy != RS_STRATEGY_CONTEXT)
         return fail(RS_ERR_INVALID_ARG, "bad strategy");
-    if ((cfg.flags & RS_FLAG_TRACE) && (agg != RS_OP_SUM_I64 || cfg.strategy != RS_STRATEGY_SIGNAL))
-        return fail(RS_ERR_UNSUPPORTED, "RS_FLAG_TRACE is built for SUM_I64 pipelines under the signal strategy");
+    if ((cfg.flags & (RS_FLAG_TRACE | RS_FLAG_PROFILE)) && (agg != RS_OP_SUM_I64 || cfg.strategy != RS_STRATEGY_SIGNAL))
+        return fail(RS_ERR_UNSUPPORTED, "RS_FLAG_TRACE / RS_FLAG_PROFILE are built for SUM_I64 pipelines under the signal strategy");
     const bool ctx_ = cfg.strategy == RS_STRATEGY_CONTEXT;
     if (ctx_ && elem == RS_U8)
         return fail(RS_ERR_UNSUPPORTED, "the context strategy is built for 4-byte elements");
@@ -422,8 +422,9 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
         Kpre.tagged = -1;
         Kpre.auto_min_len = p->auto_min_len;
     }
+    if ((pa.K.flags & RS_FLAG_TRACE) && (!p->trace || p->trace_bytes < 64))
+        return fail(RS_ERR_INVALID_ARG, "RS_FLAG_TRACE needs rs_pipeline_set_trace");
     if (pa.K.flags & RS_FLAG_TRACE) {
-        if (!p->trace || p->trace_bytes < 64) return fail(RS_ERR_INVALID_ARG, "RS_FLAG_TRACE needs rs_pipeline_set_trace");
         pa.K.trace = (uint32_t *)p->trace;
         pa.K.trace_cap = (uint32_t)std::min<uint64_t>((p->trace_bytes - 32) / 32, 0xffffffffu);
         if (cudaMemsetAsync(p->trace, 0, 32, stream) != cudaSuccess) return fail(RS_ERR_CUDA, "trace reset failed");

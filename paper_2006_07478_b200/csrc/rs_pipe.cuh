@@ -429,10 +429,12 @@ struct Pipe {
     uint32_t nchunks;
     uint32_t q_start[K + 1];       // initial queue positions (edge 0 may start at the chunk-0 pad)
     // RS_FLAG_PROFILE: cycles spent per node (0 = enumerate, 1..K+1, K+2 = TMA wait)
-    const bool prof;
+    // RS_FLAG_PROFILE cycle counters exist in the debug (TR) instantiations
+    // only: the production kernels carry no profiling code (i-cache).
+    static constexpr bool prof = TR;
 
     __device__ __forceinline__ Pipe(const KParams &p, uint8_t *smem, int lane_)
-        : P(p), lane(lane_), lt(lanemask_lt()), prof((p.flags & RS_FLAG_PROFILE) != 0) {
+        : P(p), lane(lane_), lt(lanemask_lt()) {
 
         qcap = P.qcap;
         scap = P.scap;
@@ -1039,7 +1041,7 @@ struct Pipe {
             if (lim >= (uint32_t)W) {
                 // as many full ensembles as the credit / data / space allow
                 const uint32_t nens = lim / W;
-                if constexpr (TR) trace_ens(n, in, imask, E<ei>().qh, nens * W);
+                if constexpr (TR) if (P.trace) trace_ens(n, in, imask, E<ei>().qh, nens * W);
                 run_full<n>(in, tin, imask, E<ei>().qh, nens);
                 E<ei>().qh += nens * W;
                 if (spend) E<ei>().cur -= nens * W;
@@ -1052,7 +1054,7 @@ struct Pipe {
                 const bool bounded = spend && lim == E<ei>().cur;      // ensemble <= credit
                 const bool dr = drained && lim == arem;
                 if (bounded || dr) {
-                    if constexpr (TR) trace_ens(n, in, imask, E<ei>().qh, lim);
+                    if constexpr (TR) if (P.trace) trace_ens(n, in, imask, E<ei>().qh, lim);
                     run_partial<n>(in, tin, imask, E<ei>().qh, lim);
                     E<ei>().qh += lim;
                     if (spend) E<ei>().cur -= lim;
@@ -1080,7 +1082,7 @@ struct Pipe {
                 E<ei>().xfer = false;
                 ++nsig;
                 const bool is_end = (hs.y & END_BIT) != 0;
-                if constexpr (TR) trace_event(n, is_end ? TR_END : TR_BEGIN, hs.x, 0u, 0u, 0u);
+                if constexpr (TR) if (P.trace) trace_event(n, is_end ? TR_END : TR_BEGIN, hs.x, 0u, 0u, 0u);
                 if constexpr (n <= K) {
                     if (!is_end && P.st[n - 1].op == RS_OP_PARENT_LT) set_pv(n, hs.x);
                 }

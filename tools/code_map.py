@@ -18,7 +18,10 @@ src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 rows = list(csv.reader(io.StringIO(src)))
 h = rows[1]
 ie = h.index("Instructions Executed")
+ni = h.index("stall_no_inst") if "stall_no_inst" in h else None
+sa = h.index("Warp Stall Sampling (All Samples)")
 data = [(int(r[0], 16), int(r[ie] or 0)) for r in rows[2:] if len(r) > ie]
+stall = {int(r[0], 16): (int(r[ni] or 0) if ni is not None else 0, int(r[sa] or 0)) for r in rows[2:] if len(r) > ie}
 d = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=d, capture_output=True)
 addr2line = {}
@@ -69,13 +72,21 @@ base = data[0][0]
 mx = max(n for _, n in data)
 cnt = collections.Counter()
 exe = collections.Counter()
+noi = collections.Counter()
+alls = collections.Counter()
 for a, n in data:
+    k = addr2line.get(a - base, ("?", 0))
+    f = func_of(*k) if k[0] != "?" else "?"
+    noi[f] += stall[a][0]
+    alls[f] += stall[a][1]
     if n >= thresh * mx:
-        k = addr2line.get(a - base, ("?", 0))
-        f = func_of(*k) if k[0] != "?" else "?"
         cnt[f] += 1
         exe[f] += n
 tot = sum(cnt.values())
-print(f"hot static instructions (>= {thresh} x hottest): {tot} ({tot * 16 / 1024:.1f} KB)")
+tn, ta = max(1, sum(noi.values())), max(1, sum(alls.values()))
+print(f"hot static instructions (>= {thresh} x hottest): {tot} ({tot * 16 / 1024:.1f} KB); "
+      f"no_inst stall samples {tn} of {ta} ({100 * tn / ta:.1f}%)")
+print("instr     KB   exec%  stall%  no_inst%  function")
 for f, c in cnt.most_common():
-    print(f"{c:6d} instr {c * 16 / 1024:6.1f} KB  exec {exe[f] / sum(exe.values()) * 100:5.1f}%  {f}")
+    print(f"{c:6d} {c * 16 / 1024:6.1f} {exe[f] / sum(exe.values()) * 100:6.1f} {100 * alls[f] / ta:6.1f} "
+          f"{100 * noi[f] / tn:7.1f}   {f}")
