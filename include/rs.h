@@ -59,7 +59,10 @@ typedef enum {
     RS_NODE_ENUMERATE = 1,   /* parent -> its elements, findCount = offsets  */
     RS_NODE_FILTER = 2,      /* keep or drop each item (0..1 outputs per input)          */
     RS_NODE_TRANSFORM = 3,   /* rewrite each item (exactly 1 output per input)           */
-    RS_NODE_AGGREGATE = 4    /* one result per parent (begin/run/end)         */
+    RS_NODE_AGGREGATE = 4,   /* one result per parent (begin/run/end)         */
+    RS_NODE_EMIT = 5         /* element-wise exit: every surviving item is written out with
+                                its parent's id, "stripped of their parent context"
+                                (taxi stage 2) -- rs_pipeline_run_emit */
 } rs_node_kind;
 
 /* Operations.  The paper leaves isGood() and the aggregate open (P:529,
@@ -81,7 +84,9 @@ typedef enum {
     RS_OP_SUM_I64 = 20,      /* elem i32: v0 = int64 sum                                    */
     RS_OP_SUM_F32 = 21,      /* elem f32: v0 = float sum (fp32 accumulation)               */
     RS_OP_COUNT_MIN_U32 = 22,/* elem u32: v0 = uint32 count, v1 = uint32 min (0xFFFFFFFF if none) */
-    RS_OP_COUNT_XOR64 = 23   /* elem u8 : v0 = uint64 count, v1 = uint64 xor of mix64(i<<8|byte) */
+    RS_OP_COUNT_XOR64 = 23,  /* elem u8 : v0 = uint64 count, v1 = uint64 xor of mix64(i<<8|byte) */
+    /* EMIT ops */
+    RS_OP_EMIT_VALUE = 24    /* elem i32/u32/f32: emit (value bits, region id) of each item   */
 } rs_op;
 
 typedef enum { RS_I32 = 0, RS_U32 = 1, RS_U8 = 2, RS_F32 = 3 } rs_dtype;
@@ -208,6 +213,20 @@ rs_status rs_pipeline_run(rs_pipeline *p, const void *d_elems, int64_t n_elems,
                           const int64_t *d_offsets, int64_t n_regions, const void *d_parent_ctx,
                           rs_aggregates out, void *d_ws, size_t ws_bytes, rs_stream stream);
 
+/* Element-wise exit (a pipeline whose last node is RS_NODE_EMIT): like
+ * rs_pipeline_run, but instead of per-region aggregates every item that
+ * survives the stages is written as d_values[k] (its 32-bit value) and
+ * d_regions[k] (its region j) for distinct k < *d_count.  The
+ * order of the pairs is unspecified (instances write their ensembles as they
+ * finish; within an ensemble stream order is kept).  *d_count is zeroed and
+ * then set to the number of surviving items; when it exceeds `capacity` only
+ * `capacity` pairs were written and rs_pipeline_check reports code 8.
+ * rs_pipeline_run rejects EMIT pipelines and vice versa. */
+rs_status rs_pipeline_run_emit(rs_pipeline *p, const void *d_elems, int64_t n_elems,
+                               const int64_t *d_offsets, int64_t n_regions, const void *d_parent_ctx,
+                               uint32_t *d_values, uint32_t *d_regions, uint64_t capacity, uint64_t *d_count,
+                               void *d_ws, size_t ws_bytes, rs_stream stream);
+
 /* End-to-end convenience: same as rs_pipeline_run but with HOST buffers.
  * Copies elements, offsets (and parent contexts) host->device (pinned host memory gives
  * asynchronous copies), runs, and copies the aggregates back into h_out;
@@ -231,7 +250,8 @@ rs_status rs_pipeline_profile(rs_pipeline *p, uint64_t *host16, rs_stream stream
  * Returns RS_ERR_PROTOCOL and sets *code (if non-NULL) when the device saw a
  * violated invariant: 1 = bad offsets (VALIDATE), 2 = watchdog (no progress),
  * 3 = signal queue overflow, 4 = unmatched End, 5 = queue overflow,
- * 7 = a receiver's readable limit fell behind its consumed position. */
+ * 7 = a receiver's readable limit fell behind its consumed position,
+ * 8 = RS_NODE_EMIT output capacity exceeded. */
 rs_status rs_pipeline_check(rs_pipeline *p, rs_stream stream, int32_t *code);
 
 /* Device time of the last run's kernels (needs RS_FLAG_TIMING; synchronises

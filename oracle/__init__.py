@@ -86,6 +86,8 @@ def lib():
         L.or_brute.argtypes = [i32, vp, vp, i64, vp, i32, i32, vp, vp]
         L.or_brute_range.argtypes = [i32, vp, vp, i64, i64, vp, i32, i32, vp, vp]
         L.or_node_counts.argtypes = [i32, vp, vp, i64, vp, i32, vp]
+        L.or_emit.argtypes = [i32, vp, vp, i64, vp, i32, vp, vp, i64]
+        L.or_emit.restype = i64
         L.or_interp.argtypes = [i32, vp, vp, i64, vp, i32, i32, i32, i64, i64, i64, i32, u64, i32,
                                 vp, vp, vp, vp, i64, vp]
         L.or_mix64.argtypes = [u64]
@@ -180,6 +182,22 @@ def brute(elems, offsets, stages, agg):
     if rc:
         raise OracleError(ERRORS.get(rc, rc))
     return o0, o1
+
+
+def emit(elems, offsets, stages):
+    """Element-wise exit: (values u32[n], regions
+    u32[n]) of every item surviving the stages, in stream order."""
+    elems, offsets = _prep(elems, offsets)
+    R = offsets.size - 1
+    st, keep = _stages(stages)
+    n = int(offsets[-1] - offsets[0]) if R else 0
+    v = np.zeros(max(1, n), np.uint32)
+    r = np.zeros(max(1, n), np.uint32)
+    m = lib().or_emit(DTYPES[_dtype_name(elems)], _ptr(elems), _ptr(offsets), R, C.addressof(st), len(stages),
+                      _ptr(v), _ptr(r), n)
+    if m < 0:
+        raise OracleError("bad arguments")
+    return v[:m], r[:m]
 
 
 def brute_range(elems, offsets, r0, r1, stages, agg, o0, o1):

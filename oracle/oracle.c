@@ -202,6 +202,29 @@ int or_node_counts(int dtype, const void *elems, const int64_t *off, int64_t R,
     return OR_OK;
 }
 
+/* Element-wise exit: instead of one result per parent, a
+ * stream of results derived from individual elements, "stripped of their
+ * parent context" (§4; the taxi app's second stage emits each
+ * verified pair with its line's tag, §5).  Plain definition: every
+ * item surviving the stages is emitted as (parent r, value) in stream order.
+ * Returns the number emitted (> cap: only the first cap were written).     */
+int64_t or_emit(int dtype, const void *elems, const int64_t *off, int64_t R,
+                const or_stage *st, int nst, uint32_t *out_val, uint32_t *out_reg, int64_t cap) {
+    if (check_args(dtype, elems, off, R, st, nst, OR_SUM_I64)) return -1;
+    int64_t n = 0;
+    for (int64_t r = 0; r < R; r++) {
+        for (int64_t g = off[r]; g < off[r + 1]; g++) {
+            uint32_t v = get_item(dtype, elems, g);
+            int keep = 1;
+            for (int k = 0; k < nst && keep; k++) keep = apply_stage(&st[k], &v, r);
+            if (!keep) continue;
+            if (n < cap) { out_val[n] = v; out_reg[n] = (uint32_t)r; }
+            n++;
+        }
+    }
+    return n;
+}
+
 /* ================================================================ one edge
  * Data queue Q and signal queue S between successive nodes n1 -> n2
  * (§3.1, Fig. 2a).  FIFO rings of fixed capacity.                  */

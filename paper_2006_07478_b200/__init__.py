@@ -19,9 +19,9 @@ LIB_PATH = os.environ.get("RS_LIB") or os.path.join(_HERE, "lib", "librs.so")
 # rs.h enumerations (kept in sync with include/rs.h by tests/test_abi.py)
 RS_OK, RS_ERR_INVALID_ARG, RS_ERR_INVALID_TOPOLOGY, RS_ERR_UNSUPPORTED = 0, -1, -2, -3
 RS_ERR_WORKSPACE, RS_ERR_CUDA, RS_ERR_PROTOCOL, RS_ERR_NCCL = -4, -5, -6, -7
-RS_NODE_ENUMERATE, RS_NODE_FILTER, RS_NODE_TRANSFORM, RS_NODE_AGGREGATE = 1, 2, 3, 4
+RS_NODE_ENUMERATE, RS_NODE_FILTER, RS_NODE_TRANSFORM, RS_NODE_AGGREGATE, RS_NODE_EMIT = 1, 2, 3, 4, 5
 OPS = {"none": 0, "hash_lt": 1, "lt_u32": 2, "class": 3, "parent_lt": 4, "scale_f32": 10, "affine_i32": 11,
-       "sum_i64": 20, "sum_f32": 21, "count_min_u32": 22, "count_xor64": 23}
+       "sum_i64": 20, "sum_f32": 21, "count_min_u32": 22, "count_xor64": 23, "emit_value": 24}
 DTYPES = {"i32": 0, "u32": 1, "u8": 2, "f32": 3}
 STRATEGIES = {"signal": 0, "tagged": 1, "auto": 2, "context": 3}
 STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
@@ -30,7 +30,7 @@ RS_FLAG_TRACE = 64
 TRACE_ENSEMBLE, TRACE_BEGIN, TRACE_END = 1, 2, 3
 
 EXPORTS = ["rs_config_default", "rs_pipeline_create", "rs_pipeline_workspace_bytes", "rs_pipeline_run",
-           "rs_pipeline_run_host", "rs_pipeline_stats", "rs_pipeline_profile", "rs_pipeline_check",
+           "rs_pipeline_run_host", "rs_pipeline_run_emit", "rs_pipeline_stats", "rs_pipeline_profile", "rs_pipeline_check",
            "rs_pipeline_kernel_times",
            "rs_pipeline_launches", "rs_pipeline_last_strategy",
            "rs_pipeline_geometry", "rs_pipeline_set_trace", "rs_pipeline_destroy", "rs_status_string",
@@ -80,6 +80,8 @@ def lib():
         L.rs_pipeline_workspace_bytes.argtypes = [vp, i64, i64, C.POINTER(C.c_size_t)]
         L.rs_pipeline_run.argtypes = [vp, vp, i64, vp, i64, vp, rs_aggregates, vp, C.c_size_t, vp]
         L.rs_pipeline_run_host.argtypes = [vp, vp, i64, vp, i64, vp, rs_aggregates, vp]
+        L.rs_pipeline_run_emit.argtypes = [vp, vp, i64, vp, i64, vp, vp, vp, C.c_uint64, vp, vp, C.c_size_t, vp]
+        L.rs_pipeline_run_emit.restype = i32
         L.rs_pipeline_stats.argtypes = [vp, vp, i32, vp]
         L.rs_pipeline_check.argtypes = [vp, vp, C.POINTER(C.c_int32)]
         L.rs_pipeline_profile.argtypes = [vp, vp, vp]
@@ -110,7 +112,7 @@ def lib():
         L.rs_status_string.restype = C.c_char_p
         L.rs_last_error.restype = C.c_char_p
         for name in ("rs_config_default", "rs_pipeline_create", "rs_pipeline_workspace_bytes", "rs_pipeline_run",
-                     "rs_pipeline_run_host", "rs_pipeline_stats", "rs_pipeline_check", "rs_pipeline_geometry",
+                     "rs_pipeline_run_host", "rs_pipeline_run_emit", "rs_pipeline_stats", "rs_pipeline_check", "rs_pipeline_geometry",
                      "rs_pipeline_last_strategy"):
             getattr(L, name).restype = i32
         _lib = L
@@ -144,7 +146,7 @@ def _node(spec) -> tuple:
     raise ValueError(f"unknown stage {name}")
 
 
-AGG_ELEM = {"sum_i64": "i32", "sum_f32": "f32", "count_min_u32": "u32", "count_xor64": "u8"}
+AGG_ELEM = {"sum_i64": "i32", "sum_f32": "f32", "count_min_u32": "u32", "count_xor64": "u8", "emit_value": "i32"}
 
 
 class Pipeline:
@@ -168,7 +170,7 @@ class Pipeline:
                 self._tables.append(buf)
                 tp = C.addressof(buf)
             nodes[i + 1] = rs_node(kind, op, p0, p1, tp)
-        nodes[-1] = rs_node(RS_NODE_AGGREGATE, OPS[agg], 0, 0, None)
+        nodes[-1] = rs_node(RS_NODE_EMIT if agg == "emit_value" else RS_NODE_AGGREGATE, OPS[agg], 0, 0, None)
         cfg = rs_config()
         L.rs_config_default(C.byref(cfg))
         cfg.strategy = STRATEGIES[strategy]
@@ -242,6 +244,21 @@ class Pipeline:
         _check(lib().rs_pipeline_run(self.h, elems.data_ptr() if elems.numel() else None, elems.numel(),
                                      offsets.data_ptr(), R, parent_ctx.data_ptr() if parent_ctx is not None else None,
                                      agg, ws_ptr, ws_bytes, C.c_void_p(stream.cuda_stream)))
+
+    def run_emit(self, elems, offsets, values, regions, count, workspace, stream=None, parent_ctx=None):
+        """EMIT pipelines: every surviving item -> values[k] (int32/uint32
+        tensor), regions[k] (int32 tensor), k < count[0] (int64 device tensor)."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        R = offsets.numel() - 1
+        ws_ptr = (workspace.data_ptr() + 255) & ~255
+        ws_bytes = workspace.numel() - (ws_ptr - workspace.data_ptr())
+        _check(lib().rs_pipeline_run_emit(self.h, elems.data_ptr() if elems.numel() else None, elems.numel(),
+                                          offsets.data_ptr(), R,
+                                          parent_ctx.data_ptr() if parent_ctx is not None else None,
+                                          values.data_ptr(), regions.data_ptr(), min(values.numel(), regions.numel()),
+                                          count.data_ptr(), ws_ptr, ws_bytes, C.c_void_p(stream.cuda_stream)))
 
     def run_raw(self, elems_ptr, n_elems, offsets_ptr, n_regions, out0_ptr, out1_ptr, ws_ptr, ws_bytes, stream_ptr,
                 ctx_ptr=None):

@@ -97,6 +97,7 @@ bool get_launch(const rs_pipeline *p, Launch *L) {
         case RS_OP_SUM_I64: *L = launch_agg20(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
         case RS_OP_SUM_F32: *L = launch_agg21(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
         case RS_OP_COUNT_MIN_U32: *L = launch_agg22(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
+        case RS_OP_EMIT_VALUE: *L = launch_agg24(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
         case RS_OP_COUNT_XOR64: *L = launch_agg23(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
     }
     return false;
@@ -165,11 +166,16 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     rs_config cfg;
     if (cfg_in) cfg = *cfg_in; else rs_config_default(&cfg);
     if (nodes[0].kind != RS_NODE_ENUMERATE) return fail(RS_ERR_INVALID_TOPOLOGY, "node 0 must be ENUMERATE");
-    if (nodes[n_nodes - 1].kind != RS_NODE_AGGREGATE) return fail(RS_ERR_INVALID_TOPOLOGY, "last node must be AGGREGATE");
+    if (nodes[n_nodes - 1].kind != RS_NODE_AGGREGATE && nodes[n_nodes - 1].kind != RS_NODE_EMIT)
+        return fail(RS_ERR_INVALID_TOPOLOGY, "last node must be AGGREGATE or EMIT");
+    const bool emit_ = nodes[n_nodes - 1].kind == RS_NODE_EMIT;
+    if (emit_ && nodes[n_nodes - 1].op != RS_OP_EMIT_VALUE) return fail(RS_ERR_UNSUPPORTED, "EMIT needs RS_OP_EMIT_VALUE");
+    if (!emit_ && nodes[n_nodes - 1].op == RS_OP_EMIT_VALUE) return fail(RS_ERR_INVALID_TOPOLOGY, "RS_OP_EMIT_VALUE belongs to an EMIT node");
     int nst = n_nodes - 2;
     for (int i = 1; i < n_nodes - 1; ++i) {
         if (nodes[i].kind == RS_NODE_ENUMERATE) return fail(RS_ERR_INVALID_TOPOLOGY, "nested ENUMERATE is not supported (single-level enumeration)");
-        if (nodes[i].kind == RS_NODE_AGGREGATE) return fail(RS_ERR_INVALID_TOPOLOGY, "AGGREGATE must be the last node");
+        if (nodes[i].kind == RS_NODE_AGGREGATE || nodes[i].kind == RS_NODE_EMIT)
+            return fail(RS_ERR_INVALID_TOPOLOGY, "AGGREGATE / EMIT must be the last node");
         if (nodes[i].kind != RS_NODE_FILTER && nodes[i].kind != RS_NODE_TRANSFORM)
             return fail(RS_ERR_INVALID_TOPOLOGY, "unknown node kind at position " + std::to_string(i));
     }
@@ -182,6 +188,11 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
         case RS_OP_COUNT_MIN_U32: if (elem != RS_U32) return fail(RS_ERR_UNSUPPORTED, "COUNT_MIN_U32 needs u32 elements"); break;
         case RS_OP_COUNT_XOR64:
             if (elem != RS_U8) return fail(RS_ERR_UNSUPPORTED, "COUNT_XOR64 needs u8 elements");
+            break;
+        case RS_OP_EMIT_VALUE:
+            if (elem == RS_U8) return fail(RS_ERR_UNSUPPORTED, "EMIT_VALUE needs 4-byte elements");
+            if (cfg.strategy == RS_STRATEGY_CONTEXT) return fail(RS_ERR_UNSUPPORTED, "EMIT is built for the signal and tagged strategies");
+            if (cfg.flags & (RS_FLAG_TRACE | RS_FLAG_PROFILE)) return fail(RS_ERR_UNSUPPORTED, "trace/profile are built for SUM_I64");
             break;
         default: return fail(RS_ERR_UNSUPPORTED, "unknown aggregate op");
     }
@@ -387,9 +398,15 @@ static rs_status prepare(rs_pipeline *p, const void *d_elems, int64_t n_elems, c
     return RS_OK;
 }
 
+struct EmitOut {
+    uint32_t *vals = nullptr, *regs = nullptr;
+    uint64_t cap = 0;
+    uint64_t *count = nullptr;
+};
+
 static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, const int64_t *d_offsets,
                           int64_t n_regions, const void *d_ctx, rs_aggregates out, void *d_ws, size_t ws_bytes,
-                          cudaStream_t stream) {
+                          cudaStream_t stream, const EmitOut *em = nullptr) {
     if (!p) return fail(RS_ERR_INVALID_ARG, "pipeline is NULL");
     p->launches = 0;
     if (n_regions < 0 || n_regions >= (1ll << 31)) return fail(RS_ERR_INVALID_ARG, "n_regions must be in [0, 2^31)");
@@ -417,6 +434,17 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
     if (d_ctx && ((uintptr_t)d_ctx & 3u)) return fail(RS_ERR_INVALID_ARG, "d_parent_ctx must be 4-byte aligned");
     pa.K.ctx = (const uint32_t *)d_ctx;
     pb.K.ctx = (const uint32_t *)d_ctx;
+    if ((p->agg == RS_OP_EMIT_VALUE) != (em != nullptr))
+        return fail(RS_ERR_INVALID_ARG, em ? "not an EMIT pipeline (use rs_pipeline_run)" : "EMIT pipelines run with rs_pipeline_run_emit");
+    if (em) {
+        for (KParams *k : {&pa.K, &pb.K}) {
+            k->emit_vals = em->vals;
+            k->emit_regs = em->regs;
+            k->emit_cap = em->cap;
+            k->emit_n = (unsigned long long *)em->count;
+        }
+        if (cudaMemsetAsync(em->count, 0, 8, stream) != cudaSuccess) return fail(RS_ERR_CUDA, "emit count reset failed");
+    }
     KParams Kpre = pa.K;
     if (is_auto) {
         Kpre.tagged = -1;
@@ -459,6 +487,28 @@ rs_status rs_pipeline_run(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
                           rs_stream stream) {
     if (!p) return fail(RS_ERR_INVALID_ARG, "pipeline is NULL");
     return run_impl(p, d_elems, n_elems, d_offsets, n_regions, d_parent_ctx, out, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
+rs_status rs_pipeline_run_emit(rs_pipeline *p, const void *d_elems, int64_t n_elems, const int64_t *d_offsets,
+                               int64_t n_regions, const void *d_parent_ctx, uint32_t *d_values, uint32_t *d_regions,
+                               uint64_t capacity, uint64_t *d_count, void *d_ws, size_t ws_bytes, rs_stream stream) {
+    if (!p) return fail(RS_ERR_INVALID_ARG, "pipeline is NULL");
+    if (!d_count || (capacity > 0 && (!d_values || !d_regions)))
+        return fail(RS_ERR_INVALID_ARG, "emit outputs are NULL");
+    if (((uintptr_t)d_count & 7u) != 0) return fail(RS_ERR_INVALID_ARG, "d_count must be 8-byte aligned");
+    if (n_regions == 0) {
+        if (cudaMemsetAsync(d_count, 0, 8, (cudaStream_t)stream) != cudaSuccess) return fail(RS_ERR_CUDA, "emit count reset failed");
+        return RS_OK;
+    }
+    EmitOut em;
+    em.vals = d_values;
+    em.regs = d_regions;
+    em.cap = capacity;
+    em.count = d_count;
+    static uint32_t dummy_out;                        // prepare() wants a non-null v0 (never written)
+    rs_aggregates out{d_values ? (void *)d_values : (void *)&dummy_out, nullptr};
+    return run_impl(p, d_elems, n_elems, d_offsets, n_regions, d_parent_ctx, out, d_ws, ws_bytes, (cudaStream_t)stream,
+                    &em);
 }
 
 rs_status rs_pipeline_run_host(rs_pipeline *p, const void *h_elems, int64_t n_elems, const int64_t *h_offsets,

@@ -220,6 +220,24 @@ struct AggT<23> {  // RS_OP_COUNT_XOR64 over u8 elements: (count, xor of mix64(i
     static constexpr int bytes0 = 8, bytes1 = 8;
 };
 
+template <>
+struct AggT<24> {  // RS_OP_EMIT_VALUE: element-wise exit -- no per-region fold (the EMIT node writes items)
+    static constexpr bool heavy = false;
+    static constexpr bool group = true;
+    using A = uint32_t;
+    __device__ static A id() { return 0u; }
+    __device__ static A lift(uint32_t) { return 0u; }
+    __device__ static A lift_i(uint32_t, long long) { return 0u; }
+    __device__ static A comb(A, A) { return 0u; }
+    __device__ static A sub(A, A) { return 0u; }
+    __device__ static A shfl(A a, int) { return a; }
+    __device__ static A shfl_up(A a, int) { return a; }
+    __device__ static A shfl_xor(A a, int) { return a; }
+    __device__ static void store(void *, void *, uint64_t, A) {}
+    __device__ static A load(const void *, const void *, uint64_t) { return 0u; }
+    static constexpr int bytes0 = 4, bytes1 = 0;
+};
+
 template <class AT>
 __device__ __forceinline__ typename AT::A warp_reduce(typename AT::A a) {
 #pragma unroll

@@ -49,6 +49,7 @@ constexpr int WPB = 4;              // warps (instances) per CTA (default)
 constexpr int WPB_MAX = 16;         // sequential kernel: up to 16 instances per CTA (one CTA may fill an SM)
 
 enum : uint32_t { TR_ENSEMBLE = 1, TR_BEGIN = 2, TR_END = 3 };   // trace event types (RS_FLAG_TRACE)
+enum : int32_t { ERR_EMIT_FULL = 8 };      // RS_NODE_EMIT output capacity exceeded
 enum : int32_t { ERR_OFFSETS = 1, ERR_WATCHDOG = 2, ERR_SIGFULL = 3, ERR_UNMATCHED = 4, ERR_QFULL = 5, ERR_LIMIT = 7 };
 
 struct StageP {
@@ -90,6 +91,10 @@ struct KParams {
     int32_t nst;
     StageP st[MAXK];
     const uint32_t *ctx;            // parent context, one uint32 per region (PARENT_LT), or null
+    uint32_t *emit_vals;            // RS_NODE_EMIT: emitted item values [emit_cap]
+    uint32_t *emit_regs;            //   and their regions [emit_cap]
+    unsigned long long *emit_n;     //   items emitted (may exceed emit_cap: overflow)
+    unsigned long long emit_cap;
     uint32_t *trace;                // RS_FLAG_TRACE: [0] events written, events of 8 words from word 8
     uint32_t trace_cap;             // events the buffer holds
 };
@@ -218,6 +223,7 @@ Launch launch_agg20(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, ui
 Launch launch_agg21(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
 Launch launch_agg22(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
 Launch launch_agg23(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
+Launch launch_agg24(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
 // RS_FLAG_TRACE instantiations (SUM_I64, signal strategy; defined in rs_k20.cu)
 Launch launch_agg20_trace(int K, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk);
 
@@ -259,7 +265,7 @@ uint32_t smem_for(int K, uint32_t qcap, uint32_t scap, uint32_t ring) {
 template <int AGG>
 Launch launch_for(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx = false) {
     Launch L;
-    if constexpr (AGG != 23) {      // per-lane context strategy: 4-byte (in-place) element streams
+    if constexpr (AGG != 23 && AGG != 24) {      // per-lane context strategy: 4-byte (in-place) element streams
         if (ctx) {
             L = launch_for<AGG>(K, false, fuse, qcap, scap, sblk, false);
             L.main = fuse ? pick_k<AGG, false, true, true>(K) : pick_k<AGG, false, false, true>(K);

@@ -333,6 +333,7 @@ struct Pipe {
     static constexpr int NSG = NA ? K : K + 1;        // signal rings S_0..S_{NSG-1}
     static constexpr uint32_t default_stage() { return TAG ? 256u : 512u; }
     static constexpr bool U8 = (AGG == 23);          // text stream: byte elements
+    static constexpr bool EMIT = (AGG == 24);        // element-wise exit instead of an aggregate (§8 f3)
     static constexpr uint32_t ESZ = U8 ? 1u : 4u;    // element size in the Q0 ring (bytes)
     // INPLACE (4-byte elements): every data queue Q_0..Q_NQ lives in ONE ring.
     // Positions of all edges share the ring's coordinates and each FILTER/
@@ -425,6 +426,7 @@ struct Pipe {
     long long adelta;  // text aggregate: index offset of the current part (see part_delta)
     uint32_t dkey;     // tagged text aggregate: key whose delta is cached in adelta (per lane)
     uint32_t fkept;    // fused aggregate: items that reached it (per lane; node statistics)
+    uint32_t ekey = 0; // EMIT, signal strategy: key of the open region
     long long base0, offR, off0;
     uint32_t nchunks;
     uint32_t q_start[K + 1];       // initial queue positions (edge 0 may start at the chunk-0 pad)
@@ -885,6 +887,10 @@ struct Pipe {
         acc = AT::comb(acc, part);
     }
     __device__ __forceinline__ void agg_full(const uint32_t *in, uint32_t imask, uint32_t h, uint32_t nens) {
+        if constexpr (EMIT) {
+            for (uint32_t k = 0; k < nens; ++k) emit_ens(in, nullptr, imask, h + k * W, W, OpAll{});
+            return;
+        }
         uint32_t k = 0;
         for (; k + 2 <= nens; k += 2, h += 2 * W) agg_slices<2 * IPL>(in, imask, h);
         if (k < nens) agg_slices<IPL>(in, imask, h);
@@ -894,6 +900,10 @@ struct Pipe {
     // survivors into the per-lane accumulator (isGood + a::run).
     template <class Op>
     __device__ __forceinline__ void fused_full(const uint32_t *in, uint32_t imask, uint32_t h, uint32_t nens, const Op op) {
+        if constexpr (EMIT) {
+            for (uint32_t k = 0; k < nens; ++k) emit_ens(in, nullptr, imask, h + k * W, W, op);
+            return;
+        }
         if constexpr (K == 1) {
             // single-stage pipeline: inline (no other stage code competes for the
             // instruction cache; fewer registers -> more instances per SM)
@@ -1087,7 +1097,9 @@ struct Pipe {
                     if (!is_end && P.st[n - 1].op == RS_OP_PARENT_LT) set_pv(n, hs.x);
                 }
                 if constexpr (AGGN) {
-                    if (!is_end) {               // a::begin: acc = identity
+                    if constexpr (EMIT) {
+                        if (!is_end) ekey = hs.x;   // items until End belong to this region
+                    } else if (!is_end) {        // a::begin: acc = identity
                         acc = AT::id();
                         if constexpr (U8) adelta = part_delta(hs.x);
                     } else {                     // a::end: push(acc)
@@ -1111,6 +1123,49 @@ struct Pipe {
         }
         __syncwarp();
         return prog;
+    }
+
+    // ------------------------------------------- element-wise exit (EMIT)
+    // RS_NODE_EMIT (§8 f3; "a stream of results derived from
+    // individual elements, stripped of their parent context"): every item of
+    // an ensemble that passes the node's op is written to the global output
+    // as (value, region).  One atomic per ensemble reserves the slots; the
+    // survivors are compacted into them with the same ballot/popc prefix as a
+    // filter.  Signal strategy: the region is the open one (uniform over the
+    // ensemble); tagged: each item's tag.
+    template <class Op>
+    __device__ __forceinline__ void emit_ens(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
+                                             uint32_t e, const Op op) {
+        uint32_t v[IPL], tg[IPL], mk[IPL];
+        uint32_t total = 0;
+#pragma unroll
+        for (int j = 0; j < IPL; ++j) {
+            const uint32_t idx = j * 32 + lane;
+            const bool act = idx < e;
+            v[j] = act ? in[(h + idx) & imask] : 0u;
+            tg[j] = (TAG && act) ? tin[(h + idx) & imask] : 0u;
+            const bool keep = act && op(v[j]);
+            mk[j] = __ballot_sync(kFull, keep);
+            total += __popc(mk[j]);
+        }
+        if (total == 0) return;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(P.emit_n, (unsigned long long)total);
+        base = __shfl_sync(kFull, base, 0);
+        if (base + total > P.emit_cap && lane == 0) atomicCAS((int *)&P.hdr->err, 0, ERR_EMIT_FULL);
+        const uint32_t ureg = TAG ? 0u : region_key(ekey);
+        uint32_t rel = 0;
+#pragma unroll
+        for (int j = 0; j < IPL; ++j) {
+            if ((mk[j] >> lane) & 1u) {
+                const unsigned long long pos = base + rel + __popc(mk[j] & lt);
+                if (pos < P.emit_cap) {
+                    P.emit_vals[pos] = v[j];
+                    P.emit_regs[pos] = TAG ? region_key(tg[j]) : ureg;
+                }
+            }
+            rel += __popc(mk[j]);
+        }
     }
 
     // ------------------------------------------------- trace mode (TR)
@@ -1445,7 +1500,9 @@ struct Pipe {
     __device__ __forceinline__ void run_partial(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                                 uint32_t e) {
         if constexpr (n == K + 1) {
-            if constexpr (!TAG) {
+            if constexpr (!TAG && EMIT) {
+                emit_ens(in, nullptr, imask, h, e, OpAll{});
+            } else if constexpr (!TAG) {
 #pragma unroll
                 for (int j = 0; j < IPL; ++j) {
                     const uint32_t idx = j * 32 + lane;
@@ -1455,7 +1512,9 @@ struct Pipe {
                 agg_tagged(in, tin, imask, h, e, OpAll{});
             }
         } else if constexpr (NA && n == K) {
-            if constexpr (!TAG) {
+            if constexpr (!TAG && EMIT) {
+                with_op(P.st[n - 1], pvn(n), [&](auto op) { emit_ens(in, nullptr, imask, h, e, op); });
+            } else if constexpr (!TAG) {
                 with_op(P.st[n - 1], pvn(n), [&](auto op) {
                     const FusedAcc<AT> r = fused_partial<AT, decltype(op), AGG_U8IN>(in, imask, h, e, op, adelta, P.C - 1,
                                                                                      FusedAcc<AT>{acc, fkept});
@@ -1481,6 +1540,12 @@ struct Pipe {
     template <class Op>
     __device__ __forceinline__ void agg_tagged(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                                uint32_t e, const Op op) {
+        if constexpr (EMIT) emit_ens(in, tin, imask, h, e, op);
+        else agg_tagged_fold(in, tin, imask, h, e, op);
+    }
+    template <class Op>
+    __device__ __forceinline__ void agg_tagged_fold(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
+                                                    uint32_t e, const Op op) {
 #pragma unroll
         for (int j = 0; j < IPL; ++j) {
             const int cntj = (int)e - j * 32;

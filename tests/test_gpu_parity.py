@@ -469,3 +469,50 @@ def test_auto_decides_on_call_children(rs):
     got, _, p = run_gpu(rs, vals, off, stages, "sum_i64", "auto")
     assert p.last_strategy() == "tagged"
     assert_parity(got, oracle.brute(vals, off, stages, "sum_i64"), "sum_i64")
+
+
+@pytest.mark.parametrize("strategy", ["signal", "tagged", "auto"])
+@pytest.mark.parametrize("mode", ["seq", "unfused"])
+def test_emit_elementwise_exit(rs, strategy, mode):
+    """RS_NODE_EMIT: every surviving item leaves the
+    pipeline as (value, region) -- compared with the oracle as a multiset (the
+    order across instances is unspecified), with split and empty regions,
+    transforms before the exit, and the count / overflow contract."""
+    lens = synth.lengths(6000, "zipf", seed=13, zipf_max=9000)
+    lens[::9] = 0
+    off = synth.offsets(lens, base=5)
+    vals = synth.values(int(off[-1]) + 3, "i32", seed=14)
+    for stages in ([], [("hash_lt", 0x9E3779B1, 192)], synth.sweep_stages(3) + [("affine_i32", 5, 11)]):
+        ref_v, ref_r = oracle.emit(vals, off, stages)
+        flags = rs.RS_FLAG_STATS | (rs.RS_FLAG_UNFUSED if mode == "unfused" else 0)
+        p = rs.Pipeline(stages, "emit_value", elem="i32", strategy=strategy, flags=flags, chunk=2048)
+        e = torch.from_numpy(vals).cuda()
+        o = torch.from_numpy(off).cuda()
+        R = off.size - 1
+        cap = int(ref_v.size) + 16
+        v = torch.empty(cap, dtype=torch.int32, device="cuda")
+        r = torch.empty(cap, dtype=torch.int32, device="cuda")
+        cnt = torch.empty(1, dtype=torch.int64, device="cuda")
+        ws = p.alloc_workspace(R, e.numel())
+        p.run_emit(e, o, v, r, cnt, ws)
+        torch.cuda.synchronize()
+        assert p.check() == 0
+        n = int(cnt.item())
+        assert n == ref_v.size
+        got = np.stack([r[:n].cpu().numpy().view(np.uint32), v[:n].cpu().numpy().view(np.uint32)], 1)
+        exp = np.stack([ref_r, ref_v], 1)
+        got = got[np.lexsort((got[:, 1], got[:, 0]))]
+        exp = exp[np.lexsort((exp[:, 1], exp[:, 0]))]
+        np.testing.assert_array_equal(got, exp)
+        st = p.stats()
+        assert st[0][2] == off[-1] - off[0]
+        # overflow: the count reports every survivor, check() reports code 8
+        if ref_v.size > 10:
+            small = 10
+            p.run_emit(e, o, v[:small], r[:small], cnt, ws)
+            torch.cuda.synchronize()
+            assert int(cnt.item()) == ref_v.size
+            with pytest.raises(rs.RSError):
+                p.check()
+    with pytest.raises(rs.RSError):          # an EMIT pipeline does not run through rs_pipeline_run
+        p.run(e, o, (v, None), ws)

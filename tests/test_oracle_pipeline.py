@@ -433,3 +433,27 @@ def test_parent_lt_by_construction():
     # node counts: survivors of region r at the aggregate = k_r
     kc = oracle.node_counts(vals, off, stages)
     np.testing.assert_array_equal(kc[:, 1], [np.count_nonzero(u[off[r]:off[r + 1]] < ctx[r]) for r in range(off.size - 1)])
+
+
+# ------------------------------------------------- element-wise exit (f3)
+def test_emit_matches_numpy_masks():
+    """The element-wise exit emits (parent, value) of every
+    surviving item in stream order: pinned to numpy masks -- region of each
+    element by np.repeat over the lengths, survival by a numpy predicate."""
+    lens = synth.lengths(700, "zipf", seed=2, zipf_max=300)
+    lens[::5] = 0
+    off = synth.offsets(lens, base=4)
+    u = synth.values(int(off[-1]), "u32", seed=3)
+    reg = np.repeat(np.arange(off.size - 1, dtype=np.uint32), lens)
+    seg = u[off[0]:]
+    v, r = oracle.emit(u, off, [])
+    np.testing.assert_array_equal(v, seg)
+    np.testing.assert_array_equal(r, reg)
+    b = 1 << 31
+    v, r = oracle.emit(u, off, [("lt_u32", b)])
+    m = seg < b
+    np.testing.assert_array_equal(v, seg[m])
+    np.testing.assert_array_equal(r, reg[m])
+    # a transform rewrites what is emitted: v' = a*v + c mod 2^32
+    v, r = oracle.emit(u, off, [("affine_i32", 3, 7)])
+    np.testing.assert_array_equal(v, (seg.astype(np.uint64) * 3 + 7).astype(np.uint32))
