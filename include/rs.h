@@ -86,7 +86,11 @@ typedef enum {
     RS_OP_COUNT_MIN_U32 = 22,/* elem u32: v0 = uint32 count, v1 = uint32 min (0xFFFFFFFF if none) */
     RS_OP_COUNT_XOR64 = 23,  /* elem u8 : v0 = uint64 count, v1 = uint64 xor of mix64(i<<8|byte) */
     /* EMIT ops */
-    RS_OP_EMIT_VALUE = 24    /* elem i32/u32/f32: emit (value bits, region id) of each item   */
+    RS_OP_EMIT_VALUE = 24,   /* elem i32/u32/f32: emit (value bits, region id) of each item   */
+    RS_OP_EMIT_PAIR = 25     /* elem u8 (taxi stage 2): each surviving byte that
+                                starts a well-formed "{x,y}" inside its line (open brace, 1-9
+                                digits, comma, 1-9 digits, close brace) is parsed, swapped and
+                                emitted as (y, x, line): d_values holds 2 uint32 per pair */
 } rs_op;
 
 typedef enum { RS_I32 = 0, RS_U32 = 1, RS_U8 = 2, RS_F32 = 3 } rs_dtype;

@@ -88,6 +88,8 @@ def lib():
         L.or_node_counts.argtypes = [i32, vp, vp, i64, vp, i32, vp]
         L.or_emit.argtypes = [i32, vp, vp, i64, vp, i32, vp, vp, i64]
         L.or_emit.restype = i64
+        L.or_emit_pair.argtypes = [vp, vp, i64, vp, i32, vp, vp, i64]
+        L.or_emit_pair.restype = i64
         L.or_interp.argtypes = [i32, vp, vp, i64, vp, i32, i32, i32, i64, i64, i64, i32, u64, i32,
                                 vp, vp, vp, vp, i64, vp]
         L.or_mix64.argtypes = [u64]
@@ -198,6 +200,22 @@ def emit(elems, offsets, stages):
     if m < 0:
         raise OracleError("bad arguments")
     return v[:m], r[:m]
+
+
+def emit_pair(elems, offsets, stages):
+    """Taxi stage 2: every byte surviving `stages` that starts a
+    well-formed "{x,y}" inside its line is emitted as (line, y, x).  Returns
+    (yx u32[n, 2], lines u32[n]) in stream order."""
+    elems, offsets = _prep(elems, offsets)
+    R = offsets.size - 1
+    st, keep = _stages(stages)
+    n = int(offsets[-1] - offsets[0]) // 4 + 1 if R else 1
+    yx = np.zeros((n, 2), np.uint32)
+    r = np.zeros(n, np.uint32)
+    m = lib().or_emit_pair(_ptr(elems), _ptr(offsets), R, C.addressof(st), len(stages), _ptr(yx), _ptr(r), n)
+    if m < 0 or m > n:
+        raise OracleError("bad arguments")
+    return yx[:m], r[:m]
 
 
 def brute_range(elems, offsets, r0, r1, stages, agg, o0, o1):

@@ -225,6 +225,44 @@ int64_t or_emit(int dtype, const void *elems, const int64_t *off, int64_t R,
     return n;
 }
 
+/* Taxi stage 2 (§5): a '{' that survived stage 1 is
+ * the start of a coordinate pair "{x,y}"; the stage verifies the pair is well
+ * formed -- '{', 1..9 decimal digits, ',', 1..9 digits, '}', all inside the line --
+ * parses it, swaps it and emits (line, y, x) (integers stand in
+ * for the paper's real values, reading R6).                        */
+static int parse_pair(const uint8_t *b, int64_t g, int64_t lim, uint32_t *x, uint32_t *y) {
+    uint32_t v[2] = {0, 0};
+    if (g >= lim || b[g] != '{') return 0;
+    int64_t i = g + 1;
+    for (int f = 0; f < 2; f++) {
+        int nd = 0;
+        while (i < lim && b[i] >= '0' && b[i] <= '9' && nd <= 9) { v[f] = v[f] * 10u + (uint32_t)(b[i] - '0'); nd++; i++; }
+        if (nd == 0 || nd > 9 || i >= lim) return 0;
+        if (b[i] != (f == 0 ? ',' : '}')) return 0;
+        i++;
+    }
+    *x = v[0]; *y = v[1];
+    return 1;
+}
+
+int64_t or_emit_pair(const uint8_t *elems, const int64_t *off, int64_t R, const or_stage *st, int nst,
+                     uint32_t *out_yx, uint32_t *out_reg, int64_t cap) {
+    if (check_args(OR_U8, elems, off, R, st, nst, OR_SUM_I64)) return -1;
+    int64_t n = 0;
+    for (int64_t r = 0; r < R; r++) {
+        for (int64_t g = off[r]; g < off[r + 1]; g++) {
+            uint32_t v = elems[g];
+            int keep = 1;
+            for (int k = 0; k < nst && keep; k++) keep = apply_stage(&st[k], &v, r);
+            uint32_t x, y;
+            if (!keep || !parse_pair(elems, g, off[r + 1], &x, &y)) continue;
+            if (n < cap) { out_yx[2 * n] = y; out_yx[2 * n + 1] = x; out_reg[n] = (uint32_t)r; }
+            n++;
+        }
+    }
+    return n;
+}
+
 /* ================================================================ one edge
  * Data queue Q and signal queue S between successive nodes n1 -> n2
  * (§3.1, Fig. 2a).  FIFO rings of fixed capacity.                  */

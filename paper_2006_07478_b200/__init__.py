@@ -21,7 +21,7 @@ RS_OK, RS_ERR_INVALID_ARG, RS_ERR_INVALID_TOPOLOGY, RS_ERR_UNSUPPORTED = 0, -1, 
 RS_ERR_WORKSPACE, RS_ERR_CUDA, RS_ERR_PROTOCOL, RS_ERR_NCCL = -4, -5, -6, -7
 RS_NODE_ENUMERATE, RS_NODE_FILTER, RS_NODE_TRANSFORM, RS_NODE_AGGREGATE, RS_NODE_EMIT = 1, 2, 3, 4, 5
 OPS = {"none": 0, "hash_lt": 1, "lt_u32": 2, "class": 3, "parent_lt": 4, "scale_f32": 10, "affine_i32": 11,
-       "sum_i64": 20, "sum_f32": 21, "count_min_u32": 22, "count_xor64": 23, "emit_value": 24}
+       "sum_i64": 20, "sum_f32": 21, "count_min_u32": 22, "count_xor64": 23, "emit_value": 24, "emit_pair": 25}
 DTYPES = {"i32": 0, "u32": 1, "u8": 2, "f32": 3}
 STRATEGIES = {"signal": 0, "tagged": 1, "auto": 2, "context": 3}
 STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
@@ -146,7 +146,8 @@ def _node(spec) -> tuple:
     raise ValueError(f"unknown stage {name}")
 
 
-AGG_ELEM = {"sum_i64": "i32", "sum_f32": "f32", "count_min_u32": "u32", "count_xor64": "u8", "emit_value": "i32"}
+AGG_ELEM = {"sum_i64": "i32", "sum_f32": "f32", "count_min_u32": "u32", "count_xor64": "u8", "emit_value": "i32",
+            "emit_pair": "u8"}
 
 
 class Pipeline:
@@ -170,7 +171,7 @@ class Pipeline:
                 self._tables.append(buf)
                 tp = C.addressof(buf)
             nodes[i + 1] = rs_node(kind, op, p0, p1, tp)
-        nodes[-1] = rs_node(RS_NODE_EMIT if agg == "emit_value" else RS_NODE_AGGREGATE, OPS[agg], 0, 0, None)
+        nodes[-1] = rs_node(RS_NODE_EMIT if agg.startswith("emit") else RS_NODE_AGGREGATE, OPS[agg], 0, 0, None)
         cfg = rs_config()
         L.rs_config_default(C.byref(cfg))
         cfg.strategy = STRATEGIES[strategy]
@@ -257,7 +258,8 @@ class Pipeline:
         _check(lib().rs_pipeline_run_emit(self.h, elems.data_ptr() if elems.numel() else None, elems.numel(),
                                           offsets.data_ptr(), R,
                                           parent_ctx.data_ptr() if parent_ctx is not None else None,
-                                          values.data_ptr(), regions.data_ptr(), min(values.numel(), regions.numel()),
+                                          values.data_ptr(), regions.data_ptr(),
+                                          min(values.numel() // (2 if self.agg == "emit_pair" else 1), regions.numel()),
                                           count.data_ptr(), ws_ptr, ws_bytes, C.c_void_p(stream.cuda_stream)))
 
     def run_raw(self, elems_ptr, n_elems, offsets_ptr, n_regions, out0_ptr, out1_ptr, ws_ptr, ws_bytes, stream_ptr,

@@ -97,6 +97,7 @@ bool get_launch(const rs_pipeline *p, Launch *L) {
         case RS_OP_SUM_I64: *L = launch_agg20(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
         case RS_OP_SUM_F32: *L = launch_agg21(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
         case RS_OP_COUNT_MIN_U32: *L = launch_agg22(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
+        case RS_OP_EMIT_PAIR: *L = launch_agg25(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, false); return true;
         case RS_OP_EMIT_VALUE: *L = launch_agg24(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
         case RS_OP_COUNT_XOR64: *L = launch_agg23(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
     }
@@ -169,8 +170,9 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     if (nodes[n_nodes - 1].kind != RS_NODE_AGGREGATE && nodes[n_nodes - 1].kind != RS_NODE_EMIT)
         return fail(RS_ERR_INVALID_TOPOLOGY, "last node must be AGGREGATE or EMIT");
     const bool emit_ = nodes[n_nodes - 1].kind == RS_NODE_EMIT;
-    if (emit_ && nodes[n_nodes - 1].op != RS_OP_EMIT_VALUE) return fail(RS_ERR_UNSUPPORTED, "EMIT needs RS_OP_EMIT_VALUE");
-    if (!emit_ && nodes[n_nodes - 1].op == RS_OP_EMIT_VALUE) return fail(RS_ERR_INVALID_TOPOLOGY, "RS_OP_EMIT_VALUE belongs to an EMIT node");
+    const bool emit_op = nodes[n_nodes - 1].op == RS_OP_EMIT_VALUE || nodes[n_nodes - 1].op == RS_OP_EMIT_PAIR;
+    if (emit_ && !emit_op) return fail(RS_ERR_UNSUPPORTED, "EMIT needs RS_OP_EMIT_VALUE or RS_OP_EMIT_PAIR");
+    if (!emit_ && emit_op) return fail(RS_ERR_INVALID_TOPOLOGY, "RS_OP_EMIT_* belongs to an EMIT node");
     int nst = n_nodes - 2;
     for (int i = 1; i < n_nodes - 1; ++i) {
         if (nodes[i].kind == RS_NODE_ENUMERATE) return fail(RS_ERR_INVALID_TOPOLOGY, "nested ENUMERATE is not supported (single-level enumeration)");
@@ -188,6 +190,11 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
         case RS_OP_COUNT_MIN_U32: if (elem != RS_U32) return fail(RS_ERR_UNSUPPORTED, "COUNT_MIN_U32 needs u32 elements"); break;
         case RS_OP_COUNT_XOR64:
             if (elem != RS_U8) return fail(RS_ERR_UNSUPPORTED, "COUNT_XOR64 needs u8 elements");
+            break;
+        case RS_OP_EMIT_PAIR:
+            if (elem != RS_U8) return fail(RS_ERR_UNSUPPORTED, "EMIT_PAIR needs u8 elements");
+            if (cfg.strategy == RS_STRATEGY_CONTEXT) return fail(RS_ERR_UNSUPPORTED, "EMIT is built for the signal and tagged strategies");
+            if (cfg.flags & (RS_FLAG_TRACE | RS_FLAG_PROFILE)) return fail(RS_ERR_UNSUPPORTED, "trace/profile are built for SUM_I64");
             break;
         case RS_OP_EMIT_VALUE:
             if (elem == RS_U8) return fail(RS_ERR_UNSUPPORTED, "EMIT_VALUE needs 4-byte elements");
@@ -434,7 +441,7 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
     if (d_ctx && ((uintptr_t)d_ctx & 3u)) return fail(RS_ERR_INVALID_ARG, "d_parent_ctx must be 4-byte aligned");
     pa.K.ctx = (const uint32_t *)d_ctx;
     pb.K.ctx = (const uint32_t *)d_ctx;
-    if ((p->agg == RS_OP_EMIT_VALUE) != (em != nullptr))
+    if ((p->agg == RS_OP_EMIT_VALUE || p->agg == RS_OP_EMIT_PAIR) != (em != nullptr))
         return fail(RS_ERR_INVALID_ARG, em ? "not an EMIT pipeline (use rs_pipeline_run)" : "EMIT pipelines run with rs_pipeline_run_emit");
     if (em) {
         for (KParams *k : {&pa.K, &pb.K}) {

@@ -238,6 +238,9 @@ struct AggT<24> {  // RS_OP_EMIT_VALUE: element-wise exit -- no per-region fold 
     static constexpr int bytes0 = 4, bytes1 = 0;
 };
 
+template <>
+struct AggT<25> : AggT<24> {};   // RS_OP_EMIT_PAIR: element-wise exit of parsed "{x,y}" pairs (u8)
+
 template <class AT>
 __device__ __forceinline__ typename AT::A warp_reduce(typename AT::A a) {
 #pragma unroll

@@ -224,6 +224,7 @@ Launch launch_agg21(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, ui
 Launch launch_agg22(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
 Launch launch_agg23(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
 Launch launch_agg24(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
+Launch launch_agg25(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
 // RS_FLAG_TRACE instantiations (SUM_I64, signal strategy; defined in rs_k20.cu)
 Launch launch_agg20_trace(int K, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk);
 
@@ -265,7 +266,7 @@ uint32_t smem_for(int K, uint32_t qcap, uint32_t scap, uint32_t ring) {
 template <int AGG>
 Launch launch_for(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx = false) {
     Launch L;
-    if constexpr (AGG != 23 && AGG != 24) {      // per-lane context strategy: 4-byte (in-place) element streams
+    if constexpr (AGG != 23 && AGG != 24 && AGG != 25) {      // per-lane context strategy: 4-byte (in-place) element streams
         if (ctx) {
             L = launch_for<AGG>(K, false, fuse, qcap, scap, sblk, false);
             L.main = fuse ? pick_k<AGG, false, true, true>(K) : pick_k<AGG, false, false, true>(K);

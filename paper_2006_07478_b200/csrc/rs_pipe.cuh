@@ -332,8 +332,9 @@ struct Pipe {
     static constexpr int NQ = NA ? K - 1 : K;         // shared-memory data queues Q_1..Q_NQ
     static constexpr int NSG = NA ? K : K + 1;        // signal rings S_0..S_{NSG-1}
     static constexpr uint32_t default_stage() { return TAG ? 256u : 512u; }
-    static constexpr bool U8 = (AGG == 23);          // text stream: byte elements
-    static constexpr bool EMIT = (AGG == 24);        // element-wise exit instead of an aggregate (§8 f3)
+    static constexpr bool U8 = (AGG == 23 || AGG == 25);   // text stream: byte elements
+    static constexpr bool EMIT = (AGG == 24 || AGG == 25); // element-wise exit instead of an aggregate (§8 f3)
+    static constexpr bool PAIR = (AGG == 25);        // taxi stage 2: parse the pair at each surviving open brace
     static constexpr uint32_t ESZ = U8 ? 1u : 4u;    // element size in the Q0 ring (bytes)
     // INPLACE (4-byte elements): every data queue Q_0..Q_NQ lives in ONE ring.
     // Positions of all edges share the ring's coordinates and each FILTER/
@@ -1133,18 +1134,58 @@ struct Pipe {
     // survivors are compacted into them with the same ballot/popc prefix as a
     // filter.  Signal strategy: the region is the open one (uniform over the
     // ensemble); tagged: each item's tag.
+    // Taxi stage 2: the open brace at global byte index g starts a
+    // well-formed pair iff it reads '{' D{1,9} ',' D{1,9} '}' before the line
+    // end `lim` (reading R6); x, y are its fields.
+    __device__ __forceinline__ bool parse_pair(long long g, long long lim, uint32_t &x, uint32_t &y) const {
+        const uint8_t *b = P.elems;
+        if (g >= lim || b[g] != '{') return false;
+        long long i = g + 1;
+        uint32_t f[2] = {0u, 0u};
+#pragma unroll 1
+        for (int k = 0; k < 2; ++k) {
+            int nd = 0;
+            uint8_t c = i < lim ? b[i] : 0;
+            while (i < lim && c >= '0' && c <= '9' && nd <= 9) {
+                f[k] = f[k] * 10u + (uint32_t)(c - '0');
+                ++nd;
+                ++i;
+                c = i < lim ? b[i] : 0;
+            }
+            if (nd == 0 || nd > 9 || i >= lim || c != (k == 0 ? ',' : '}')) return false;
+            ++i;
+        }
+        x = f[0];
+        y = f[1];
+        return true;
+    }
+    // First element of the chunk a part (key) lies in: positions within a
+    // chunk are carried in the byte items (item >> 8), see load_item.
+    __device__ __forceinline__ long long chunk_base(uint32_t key) const {
+        const long long k = (key & SLOT) ? (long long)((key & ~SLOT) >> 1) : (P.off[key] - base0) / P.C;
+        return base0 + k * (long long)P.C;
+    }
+
     template <class Op>
     __device__ __forceinline__ void emit_ens(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                              uint32_t e, const Op op) {
-        uint32_t v[IPL], tg[IPL], mk[IPL];
+        uint32_t v[IPL], tg[IPL], mk[IPL], px[IPL], py[IPL];
         uint32_t total = 0;
 #pragma unroll
         for (int j = 0; j < IPL; ++j) {
             const uint32_t idx = j * 32 + lane;
             const bool act = idx < e;
-            v[j] = act ? in[(h + idx) & imask] : 0u;
+            v[j] = act ? agg_load(in, h + idx, imask) : 0u;
             tg[j] = (TAG && act) ? tin[(h + idx) & imask] : 0u;
-            const bool keep = act && op(v[j]);
+            bool keep = act && op(v[j]);
+            px[j] = py[j] = 0u;
+            if constexpr (PAIR) {
+                if (keep) {
+                    const uint32_t key = TAG ? tg[j] : ekey;
+                    const uint32_t r = region_key(key);
+                    keep = parse_pair(chunk_base(key) + (long long)(v[j] >> 8), P.off[r + 1], px[j], py[j]);
+                }
+            }
             mk[j] = __ballot_sync(kFull, keep);
             total += __popc(mk[j]);
         }
@@ -1160,7 +1201,12 @@ struct Pipe {
             if ((mk[j] >> lane) & 1u) {
                 const unsigned long long pos = base + rel + __popc(mk[j] & lt);
                 if (pos < P.emit_cap) {
-                    P.emit_vals[pos] = v[j];
+                    if constexpr (PAIR) {             // swapped: (y, x)
+                        P.emit_vals[2 * pos] = py[j];
+                        P.emit_vals[2 * pos + 1] = px[j];
+                    } else {
+                        P.emit_vals[pos] = v[j];
+                    }
                     P.emit_regs[pos] = TAG ? region_key(tg[j]) : ureg;
                 }
             }

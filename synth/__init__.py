@@ -123,6 +123,57 @@ def text(N: int, seed: int = 0, line_mean: float = 1397.0, brace_per_line: float
     return b, off
 
 
+def taxi(n_lines: int, seed: int = 0, pairs_mean: int = 45, line_mean: int = 1397):
+    """Taxi-like corpus (lines of text holding "{x,y}" coordinate
+    pairs, ~45 pairs and ~1397 chars per line).  The filler between pairs is
+    letters and spaces only, so every '{' is a generated pair start.  About
+    10% of the pairs are malformed ("{x;y}", "{x,}", "{,y}", "{x,y" at the line
+    end, 10-digit fields); "{{x,y}" holds one well-formed pair.  Returns
+    (bytes u8[N], offsets int64[R+1], expected) where expected lists
+    (line, y, x) of every well-formed pair in stream order -- the second
+    stage's result by construction."""
+    g = _rng(seed)
+    letters = np.frombuffer(b"abcdefghijklmnopqrstuvwxyz      ", np.uint8)
+    out, offs, exp = [], [0], []
+    pos = 0
+    for ln in range(n_lines):
+        k = int(g.poisson(pairs_mean))
+        fill = max(1, (line_mean - 14 * k) // (k + 1))
+        parts = []
+        for i in range(k + 1):
+            parts.append(letters[g.integers(0, letters.size, int(g.integers(1, 2 * fill + 1)))].tobytes())
+            if i == k:
+                break
+            x, y = int(g.integers(0, 10 ** int(g.integers(1, 7)))), int(g.integers(0, 10 ** int(g.integers(1, 7))))
+            kind = int(g.integers(0, 100))
+            if kind < 90:
+                parts.append(b"{%d,%d}" % (x, y))
+                exp.append((ln, y, x))
+            elif kind < 92:
+                parts.append(b"{%d;%d}" % (x, y))
+            elif kind < 94:
+                parts.append(b"{%d,}" % x)
+            elif kind < 96:
+                parts.append(b"{,%d}" % y)
+            elif kind < 98:
+                parts.append(b"{%d,%d}" % (x + 10 ** 9, y))          # 10-digit field
+            else:
+                parts.append(b"{{%d,%d}" % (x, y))
+                exp.append((ln, y, x))
+        if ln % 17 == 5 and k > 0:                                    # a pair cut by the line end
+            parts.append(b"{%d,%d" % (7, 8))
+        line = b"".join(parts) + b"\n"
+        out.append(line)
+        pos += len(line)
+        offs.append(pos)
+    b = np.frombuffer(b"".join(out), np.uint8).copy()
+    return b, np.array(offs, np.int64), np.array(exp, np.uint32).reshape(-1, 3)
+
+
+def taxi_stages():
+    return [("class", class_table(b"{"))]
+
+
 def tiny(seed: int = 0x5EED + 1):
     """D1: 1000 parents, 1-64 children each, int32, 2 int filters, SUM_I64."""
     lens = lengths(1000, "uniform", lo=1, hi=64, seed=seed)

@@ -516,3 +516,40 @@ def test_emit_elementwise_exit(rs, strategy, mode):
                 p.check()
     with pytest.raises(rs.RSError):          # an EMIT pipeline does not run through rs_pipeline_run
         p.run(e, o, (v, None), ws)
+
+
+@pytest.mark.parametrize("strategy", ["signal", "tagged"])
+@pytest.mark.parametrize("mode", ["seq", "unfused"])
+@pytest.mark.parametrize("stage1", [True, False])
+def test_taxi_two_stage(rs, strategy, mode, stage1):
+    """The taxi-style two-stage app: lines of text are
+    the regions; stage 1 keeps the '{' bytes (CLASS), stage 2 verifies and
+    parses each "{x,y}" (reading from the byte stream, so pairs may cross
+    chunk boundaries), swaps it and emits (line, y, x).  Compared as a
+    multiset with the oracle and with the pairs the corpus generator wrote."""
+    b, off, exp = synth.taxi(800, seed=21)
+    b = np.concatenate([np.full(3, ord("x"), np.uint8), b])     # unaligned stream start
+    off = off + 3
+    stages = synth.taxi_stages() if stage1 else []
+    yx, r = oracle.emit_pair(b, off, stages)
+    np.testing.assert_array_equal(np.stack([r, yx[:, 0], yx[:, 1]], 1), exp)
+    flags = rs.RS_FLAG_STATS | (rs.RS_FLAG_UNFUSED if mode == "unfused" else 0)
+    p = rs.Pipeline(stages, "emit_pair", strategy=strategy, flags=flags, chunk=2048)
+    e = torch.from_numpy(b).cuda()
+    o = torch.from_numpy(off).cuda()
+    R = off.size - 1
+    cap = exp.shape[0] + 8
+    v = torch.empty(2 * cap, dtype=torch.int32, device="cuda")
+    rg = torch.empty(cap, dtype=torch.int32, device="cuda")
+    cnt = torch.empty(1, dtype=torch.int64, device="cuda")
+    ws = p.alloc_workspace(R, e.numel())
+    p.run_emit(e, o, v, rg, cnt, ws)
+    torch.cuda.synchronize()
+    assert p.check() == 0
+    n = int(cnt.item())
+    assert n == exp.shape[0]
+    vv = v[:2 * n].cpu().numpy().view(np.uint32).reshape(n, 2)
+    got = np.stack([rg[:n].cpu().numpy().view(np.uint32), vv[:, 0], vv[:, 1]], 1)
+    got = got[np.lexsort((got[:, 2], got[:, 1], got[:, 0]))]
+    ref = exp[np.lexsort((exp[:, 2], exp[:, 1], exp[:, 0]))]
+    np.testing.assert_array_equal(got, ref)

@@ -457,3 +457,16 @@ def test_emit_matches_numpy_masks():
     # a transform rewrites what is emitted: v' = a*v + c mod 2^32
     v, r = oracle.emit(u, off, [("affine_i32", 3, 7)])
     np.testing.assert_array_equal(v, (seg.astype(np.uint64) * 3 + 7).astype(np.uint32))
+
+
+def test_emit_pair_by_construction():
+    """Taxi stage 2: the pairs the oracle parses, verifies and
+    swaps are exactly the well-formed ones the corpus generator wrote (its
+    malformed variants -- ';', missing fields, 10-digit fields, a pair cut by
+    the line end -- are dropped; "{{x,y}" yields its inner pair)."""
+    b, off, exp = synth.taxi(300, seed=7)
+    yx, r = oracle.emit_pair(b, off, synth.taxi_stages())
+    np.testing.assert_array_equal(np.stack([r, yx[:, 0], yx[:, 1]], 1), exp)
+    # without stage 1 every byte is tried: the same pairs (only '{' can start one)
+    yx2, r2 = oracle.emit_pair(b, off, [])
+    np.testing.assert_array_equal(np.stack([r2, yx2[:, 0], yx2[:, 1]], 1), exp)
