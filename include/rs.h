@@ -103,6 +103,10 @@ typedef enum {
                                 computes its own region; no tags in the queues.  4-byte
                                 elements, sequential scheduler (signal_cap 0 = 32; a fuller
                                 boundary queue cuts ensembles, reading R3). */
+    RS_STRATEGY_HYBRID = 4,  /* per-stage strategy (§8 f1): signals up to
+                                cfg.tag_from, per-item tags from there on -- the paper's best
+                                taxi variant (signal stage 1, tags in stage 2).  SUM_I64 (i32) and
+                                EMIT_PAIR (u8) pipelines; bit-identical results. */
     RS_STRATEGY_AUTO = 2     /* choice made per run, transparently (§8 f1):
                                 signal when the call's mean region length
                                 (d_offsets[n_regions] - d_offsets[0]) / n_regions is at least
@@ -163,6 +167,11 @@ typedef struct {
     uint32_t auto_min_len;   /* RS_STRATEGY_AUTO: mean children per region at and above which the
                                 signal strategy runs; 0 = the crossover measured on B200 for the
                                 pipeline's stage count */
+    uint32_t tag_from;       /* RS_STRATEGY_HYBRID: the first edge that carries tags (edge e joins
+                                node e to node e+1; edge 0 leaves ENUMERATE).  Edges before it are
+                                signal-delimited, node tag_from converts (consumes Begin/End, tags
+                                its outputs with the open region).  1 .. (stages - 1) with the
+                                fused aggregate, 1 .. stages with RS_FLAG_UNFUSED. */
 } rs_config;
 
 /* Per-node occupancy counters (§2.2, §5).  Node 0 is the

@@ -23,7 +23,7 @@ RS_NODE_ENUMERATE, RS_NODE_FILTER, RS_NODE_TRANSFORM, RS_NODE_AGGREGATE, RS_NODE
 OPS = {"none": 0, "hash_lt": 1, "lt_u32": 2, "class": 3, "parent_lt": 4, "scale_f32": 10, "affine_i32": 11,
        "sum_i64": 20, "sum_f32": 21, "count_min_u32": 22, "count_xor64": 23, "emit_value": 24, "emit_pair": 25}
 DTYPES = {"i32": 0, "u32": 1, "u8": 2, "f32": 3}
-STRATEGIES = {"signal": 0, "tagged": 1, "auto": 2, "context": 3}
+STRATEGIES = {"signal": 0, "tagged": 1, "auto": 2, "context": 3, "hybrid": 4}
 STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
 RS_FLAG_STATS, RS_FLAG_VALIDATE, RS_FLAG_TIMING, RS_FLAG_RESERVED8, RS_FLAG_PROFILE, RS_FLAG_UNFUSED = 1, 2, 4, 8, 16, 32
 RS_FLAG_TRACE = 64
@@ -52,7 +52,8 @@ class rs_node(C.Structure):
 class rs_config(C.Structure):
     _fields_ = [("strategy", C.c_int32), ("simd_width", C.c_uint32), ("queue_cap", C.c_uint32),
                 ("signal_cap", C.c_uint32), ("grid", C.c_int32), ("chunk", C.c_uint32),
-                ("flags", C.c_uint32), ("q0_stage", C.c_uint32), ("auto_min_len", C.c_uint32)]
+                ("flags", C.c_uint32), ("q0_stage", C.c_uint32), ("auto_min_len", C.c_uint32),
+                ("tag_from", C.c_uint32)]
 
 
 class rs_node_stats(C.Structure):
@@ -155,7 +156,7 @@ class Pipeline:
     ``agg``: aggregate op name.  Node list = [ENUMERATE] + stages + [AGGREGATE]."""
 
     def __init__(self, stages, agg, elem=None, strategy="signal", queue_cap=0, signal_cap=0, grid=0,
-                 chunk=0, flags=RS_FLAG_STATS, simd_width=128, q0_stage=0, auto_min_len=0):
+                 chunk=0, flags=RS_FLAG_STATS, simd_width=128, q0_stage=0, auto_min_len=0, tag_from=0):
         L = lib()
         self.stages = list(stages)
         self.agg = agg
@@ -185,6 +186,7 @@ class Pipeline:
         cfg.flags = flags
         cfg.q0_stage = q0_stage
         cfg.auto_min_len = auto_min_len
+        cfg.tag_from = tag_from
         h = C.c_void_p()
         _check(L.rs_pipeline_create(nodes, len(self.stages) + 2, DTYPES[self.elem], C.byref(cfg), C.byref(h)))
         self.h = h

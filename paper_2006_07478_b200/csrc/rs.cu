@@ -88,6 +88,16 @@ uint32_t auto_default(int nst) {
 }
 
 bool get_launch(const rs_pipeline *p, Launch *L) {
+    if (p->cfg.strategy == RS_STRATEGY_HYBRID) {
+        const bool fuse = (p->cfg.flags & RS_FLAG_UNFUSED) == 0;
+        if (p->agg == RS_OP_SUM_I64)
+            *L = launch_agg20_hybrid(p->nst, fuse, (int)p->cfg.tag_from, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage);
+        else if (p->agg == RS_OP_EMIT_PAIR)
+            *L = launch_agg25_hybrid(p->nst, fuse, (int)p->cfg.tag_from, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage);
+        else
+            return false;
+        return L->main != nullptr;
+    }
     if (p->cfg.flags & (RS_FLAG_TRACE | RS_FLAG_PROFILE)) {    // the debug instantiations
         *L = launch_agg20_trace(p->nst, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap,
                                 p->cfg.q0_stage);
@@ -156,6 +166,7 @@ rs_status rs_config_default(rs_config *cfg) {
     cfg->flags = RS_FLAG_STATS;
     cfg->q0_stage = 0;
     cfg->auto_min_len = 0;
+    cfg->tag_from = 0;
     return RS_OK;
 }
 
@@ -232,8 +243,18 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
         *out = p;
         return RS_OK;
     }
-    if (cfg.strategy != RS_STRATEGY_SIGNAL && cfg.strategy != RS_STRATEGY_TAGGED && cfg.strategy != RS_STRATEGY_CONTEXT)
+    if (cfg.strategy != RS_STRATEGY_SIGNAL && cfg.strategy != RS_STRATEGY_TAGGED && cfg.strategy != RS_STRATEGY_CONTEXT &&
+        cfg.strategy != RS_STRATEGY_HYBRID)
         return fail(RS_ERR_INVALID_ARG, "bad strategy");
+    if (cfg.strategy == RS_STRATEGY_HYBRID) {
+        const int age = (cfg.flags & RS_FLAG_UNFUSED) ? nst : nst - 1;   // the aggregating node's input edge
+        if (agg != RS_OP_SUM_I64 && agg != RS_OP_EMIT_PAIR)
+            return fail(RS_ERR_UNSUPPORTED, "RS_STRATEGY_HYBRID is built for SUM_I64 and EMIT_PAIR pipelines");
+        if ((int)cfg.tag_from < 1 || (int)cfg.tag_from > age)
+            return fail(RS_ERR_INVALID_ARG, "tag_from must be in 1 .. " + std::to_string(age) +
+                                                " (stages - 1 fused, stages unfused)");
+        if (cfg.flags & (RS_FLAG_TRACE | RS_FLAG_PROFILE)) return fail(RS_ERR_UNSUPPORTED, "trace/profile are built for the signal strategy");
+    }
     if ((cfg.flags & (RS_FLAG_TRACE | RS_FLAG_PROFILE)) && (agg != RS_OP_SUM_I64 || cfg.strategy != RS_STRATEGY_SIGNAL))
         return fail(RS_ERR_UNSUPPORTED, "RS_FLAG_TRACE / RS_FLAG_PROFILE are built for SUM_I64 pipelines under the signal strategy");
     const bool ctx_ = cfg.strategy == RS_STRATEGY_CONTEXT;
@@ -252,7 +273,7 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     // ring amortises the scheduler, the tag ring doubles the tagged footprint
     // (profiles/r1_tuning.txt).
     const bool inplace = elem != RS_U8;
-    const bool tagged_ = cfg.strategy == RS_STRATEGY_TAGGED;
+    const bool tagged_ = cfg.strategy == RS_STRATEGY_TAGGED || cfg.strategy == RS_STRATEGY_HYBRID;
     if (cfg.queue_cap == 0) cfg.queue_cap = inplace ? (tagged_ ? 16 * W : 32 * W) : (nst_ >= 2 ? 8 * W : 16 * W);
     if (cfg.signal_cap == 0)
         cfg.signal_cap = inplace ? 32 : (nst_ >= 2 ? 64 : 128);   // (context strategy: profiles/r1_tuning.txt)
@@ -399,7 +420,7 @@ static rs_status prepare(rs_pipeline *p, const void *d_elems, int64_t n_elems, c
     K.ring0 = L.ring0;
     K.esize = p->elem == RS_U8 ? 1u : 4u;
     K.flags = p->cfg.flags;
-    K.tagged = p->cfg.strategy == RS_STRATEGY_TAGGED;
+    K.tagged = p->cfg.strategy == RS_STRATEGY_TAGGED || p->cfg.strategy == RS_STRATEGY_HYBRID;
     K.nst = p->nst;
     std::memcpy(K.st, p->st, sizeof K.st);
     return RS_OK;

@@ -1,0 +1,9 @@
+// rs_k20h.cu — RS_STRATEGY_HYBRID instantiations for aggregate op 20
+// (per-stage strategy: signals up to a stage, tags from it on; rs_pipe.cuh HYB).
+#include "rs_kern.cuh"
+
+namespace rsk {
+Launch launch_agg20_hybrid(int K, bool fuse, int hyb, uint32_t qcap, uint32_t scap, uint32_t sblk) {
+    return launch_hybrid<20>(K, fuse, hyb, qcap, scap, sblk);
+}
+}  // namespace rsk

@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <type_traits>
 
 using namespace rs;
 
@@ -85,7 +86,7 @@ struct KParams {
     uint32_t ring0;                 // Q0 ring capacity in elements (sequential kernel; in-place: all queues)
     uint32_t esize;                 // element size in bytes (1 = u8 text, else 4)
     uint32_t flags;
-    int32_t tagged;                 // 1 tagged; -1 = AUTO (the prepass decides, see k_prepass)
+    int32_t tagged;                 // 1 tagged (or hybrid: the aggregate folds by tag); -1 = AUTO (the prepass decides)
     int32_t auto_sel;               // AUTO: 0 always run; 1 = run iff hdr->sel == 0; 2 = iff hdr->sel == 1
     uint32_t auto_min_len;          // AUTO: signal iff children >= auto_min_len * regions
     int32_t nst;
@@ -225,10 +226,81 @@ Launch launch_agg22(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, ui
 Launch launch_agg23(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
 Launch launch_agg24(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
 Launch launch_agg25(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
-// RS_FLAG_TRACE instantiations (SUM_I64, signal strategy; defined in rs_k20.cu)
+// RS_FLAG_TRACE instantiations (SUM_I64, signal strategy; defined in rs_k20t.cu)
 Launch launch_agg20_trace(int K, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk);
+// RS_STRATEGY_HYBRID instantiations (edges >= hyb carry tags; rs_k20h.cu, rs_k25h.cu)
+Launch launch_agg20_hybrid(int K, bool fuse, int hyb, uint32_t qcap, uint32_t scap, uint32_t sblk);
+Launch launch_agg25_hybrid(int K, bool fuse, int hyb, uint32_t qcap, uint32_t scap, uint32_t sblk);
 
 #ifndef RS_HOST_ONLY
+// Hybrid kernels: K stages, edges >= hyb tagged (1 <= hyb <= the aggregating
+// node's input edge: K - 1 fused, K unfused).
+template <int AGG, bool FUSE, int K>
+KernelFn pick_hyb_k(int hyb) {
+    if constexpr (K >= 1) {
+        if (hyb == 1 && (!FUSE || K >= 2)) return k_pipeline<K, AGG, false, FUSE, false, false, 1>;
+    }
+    if constexpr (K >= 2) {
+        if (hyb == 2 && (!FUSE || K >= 3)) return k_pipeline<K, AGG, false, FUSE, false, false, 2>;
+    }
+    if constexpr (K >= 3) {
+        if (hyb == 3 && (!FUSE || K >= 4)) return k_pipeline<K, AGG, false, FUSE, false, false, 3>;
+    }
+    if constexpr (K >= 4 && !FUSE) {
+        if (hyb == 4) return k_pipeline<K, AGG, false, FUSE, false, false, 4>;
+    }
+    return nullptr;
+}
+template <int AGG, bool FUSE>
+KernelFn pick_hyb(int K, int hyb) {
+    switch (K) {
+        case 1: return pick_hyb_k<AGG, FUSE, 1>(hyb);
+        case 2: return pick_hyb_k<AGG, FUSE, 2>(hyb);
+        case 3: return pick_hyb_k<AGG, FUSE, 3>(hyb);
+        case 4: return pick_hyb_k<AGG, FUSE, 4>(hyb);
+    }
+    return nullptr;
+}
+// ring and shared-memory size of a hybrid kernel (tag ring + signal rings)
+template <int AGG, bool FUSE, int K, int HYB>
+void hyb_sizes(uint32_t sblk, uint32_t qcap, uint32_t scap, uint32_t &ring, uint32_t &bytes) {
+    using PP = Pipe<K, AGG, false, FUSE, false, false, HYB>;
+    ring = PP::ring_for(sblk, qcap);
+    bytes = PP::smem_bytes(qcap, scap, ring);
+}
+template <int AGG>
+Launch launch_hybrid(int K, bool fuse, int hyb, uint32_t qcap, uint32_t scap, uint32_t sblk) {
+    Launch L;
+    L.pre = k_prepass<AGG>;
+    L.fix = k_fixup<AGG>;
+    L.out_bytes0 = AggT<AGG>::bytes0;
+    L.out_bytes1 = AggT<AGG>::bytes1;
+    L.main = fuse ? pick_hyb<AGG, true>(K, hyb) : pick_hyb<AGG, false>(K, hyb);
+    // the hybrid instance holds the tag ring and the signal rings
+    uint32_t ring = 0, bytes = 0;
+    auto sz = [&](auto kk, auto hh) {
+        constexpr int KK = decltype(kk)::value, HH = decltype(hh)::value;
+        if (fuse) hyb_sizes<AGG, true, KK, HH>(sblk, qcap, scap, ring, bytes);
+        else hyb_sizes<AGG, false, KK, HH>(sblk, qcap, scap, ring, bytes);
+    };
+    using std::integral_constant;
+    switch (K * 8 + hyb) {
+        case 1 * 8 + 1: sz(integral_constant<int, 1>{}, integral_constant<int, 1>{}); break;
+        case 2 * 8 + 1: sz(integral_constant<int, 2>{}, integral_constant<int, 1>{}); break;
+        case 2 * 8 + 2: sz(integral_constant<int, 2>{}, integral_constant<int, 2>{}); break;
+        case 3 * 8 + 1: sz(integral_constant<int, 3>{}, integral_constant<int, 1>{}); break;
+        case 3 * 8 + 2: sz(integral_constant<int, 3>{}, integral_constant<int, 2>{}); break;
+        case 3 * 8 + 3: sz(integral_constant<int, 3>{}, integral_constant<int, 3>{}); break;
+        case 4 * 8 + 1: sz(integral_constant<int, 4>{}, integral_constant<int, 1>{}); break;
+        case 4 * 8 + 2: sz(integral_constant<int, 4>{}, integral_constant<int, 2>{}); break;
+        case 4 * 8 + 3: sz(integral_constant<int, 4>{}, integral_constant<int, 3>{}); break;
+        case 4 * 8 + 4: sz(integral_constant<int, 4>{}, integral_constant<int, 4>{}); break;
+    }
+    L.ring0 = ring;
+    L.inst_bytes = bytes;
+    return L;
+}
+
 template <int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false>
 KernelFn pick_k(int K) {
     switch (K) {

@@ -324,13 +324,21 @@ struct Chunk {
 // (survivors before it), and the aggregate gives each lane the key of the last
 // boundary at or before its item -- the context computed per lane instead of
 // stored with the items.
-template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false>
+template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false, int HYB = 0>
 struct Pipe {
     using AT = AggT<AGG>;
     using A = typename AT::A;
     static constexpr bool NA = FUSE && K >= 1;        // aggregate fused into node K
     static constexpr int NQ = NA ? K - 1 : K;         // shared-memory data queues Q_1..Q_NQ
     static constexpr int NSG = NA ? K : K + 1;        // signal rings S_0..S_{NSG-1}
+    // Per-stage hybrid (§8 f1; the paper's best taxi variant signals through
+    // stage 1 and tags from stage 2 on): HYB >= 1 makes
+    // edges 0..HYB-1 signal-delimited and edges HYB.. tagged; node HYB
+    // converts -- it consumes Begin/End and stamps its outputs with the open
+    // region's key (uniform over each of its ensembles).
+    static constexpr bool TAGANY = TAG || HYB > 0;   // a tag ring exists
+    template <int e> static constexpr bool TGE = TAG || (HYB > 0 && e >= HYB);   // edge e carries tags
+    static constexpr int AGE = NA ? K - 1 : K;       // the aggregating node's input edge
     static constexpr uint32_t default_stage() { return TAG ? 256u : 512u; }
     static constexpr bool U8 = (AGG == 23 || AGG == 25);   // text stream: byte elements
     static constexpr bool EMIT = (AGG == 24 || AGG == 25); // element-wise exit instead of an aggregate (§8 f3)
@@ -395,16 +403,16 @@ struct Pipe {
     static constexpr uint32_t NQS = INPLACE ? 0 : NQ;   // separate shared-memory queues
     template <int e> __device__ __forceinline__ uint32_t *Q() const {
         if constexpr (e == 0 || INPLACE) return reinterpret_cast<uint32_t *>(base + HDR);
-        else return reinterpret_cast<uint32_t *>(base + HDR + q0_bytes(ring0) + (TAG ? ring0 * 4 : 0) +
-                                                 (e - 1) * qcap * 4 * (TAG ? 2 : 1));
+        else return reinterpret_cast<uint32_t *>(base + HDR + q0_bytes(ring0) + (TAGANY ? ring0 * 4 : 0) +
+                                                 (e - 1) * qcap * 4 * (TAGANY ? 2 : 1));
     }
     template <int e> __device__ __forceinline__ uint32_t *T() const {
-        if constexpr (!TAG) return nullptr;
+        if constexpr (!TAGANY) return nullptr;
         else if constexpr (e == 0 || INPLACE) return reinterpret_cast<uint32_t *>(base + HDR + q0_bytes(ring0));
         else return Q<e>() + qcap;
     }
     template <int e> __device__ __forceinline__ uint2 *S() const {
-        return reinterpret_cast<uint2 *>(base + HDR + q0_bytes(ring0) + (TAG ? ring0 * 4 : 0) + NQS * qcap * 4 * (TAG ? 2 : 1)) +
+        return reinterpret_cast<uint2 *>(base + HDR + q0_bytes(ring0) + (TAGANY ? ring0 * 4 : 0) + NQS * qcap * 4 * (TAGANY ? 2 : 1)) +
                e * scap;
     }
     // ring index mask of edge e's queue
@@ -428,6 +436,7 @@ struct Pipe {
     uint32_t dkey;     // tagged text aggregate: key whose delta is cached in adelta (per lane)
     uint32_t fkept;    // fused aggregate: items that reached it (per lane; node statistics)
     uint32_t ekey = 0; // EMIT, signal strategy: key of the open region
+    uint32_t ckey = 0; // hybrid converter node: key of the open region
     long long base0, offR, off0;
     uint32_t nchunks;
     uint32_t q_start[K + 1];       // initial queue positions (edge 0 may start at the chunk-0 pad)
@@ -474,7 +483,7 @@ struct Pipe {
     }
 
     __host__ __device__ static constexpr uint32_t smem_bytes(uint32_t qcap, uint32_t scap, uint32_t ring) {
-        return HDR + q0_bytes(ring) + (TAG ? ring * 4 : 0) + NQS * qcap * 4 * (TAG ? 2 : 1) +
+        return HDR + q0_bytes(ring) + (TAGANY ? ring * 4 : 0) + NQS * qcap * 4 * (TAGANY ? 2 : 1) +
                (TAG ? 0 : NSG * scap * 8);
     }
     // Ring capacity: 4 TMA stages; in-place, the configured queue capacity
@@ -843,10 +852,18 @@ struct Pipe {
     template <int n, class Op>
     __device__ __forceinline__ void filter_full(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                                 uint32_t nens, const Op op) {
-        const uint32_t tl = filter_batch<TAG, Op, U8 && n == 1>(in, tin, imask, h, nens, Q<n>(), T<n>(), qm<n>(),
-                                                               E<n>().qt, op, lt, P.C - 1);
+        const uint32_t tl = filter_batch<TGE<n - 1>, Op, U8 && n == 1>(in, tin, imask, h, nens, Q<n>(), T<n>(), qm<n>(),
+                                                                      E<n>().qt, op, lt, P.C - 1);
+        if constexpr (HYB > 0 && n == HYB) stamp_tags<n>(E<n>().qt, tl);
         E<n>().sent += tl - E<n>().qt;
         E<n>().qt = tl;
+    }
+    // hybrid converter: its outputs [t0, t1) carry the open region's key
+    template <int n>
+    __device__ __forceinline__ void stamp_tags(uint32_t t0, uint32_t t1) {
+        uint32_t *tq = T<n>();
+        for (uint32_t i = t0 + lane; i - t0 < t1 - t0; i += 32) tq[i & qm<n>()] = ckey;
+        __syncwarp();
     }
 
     static constexpr bool AGG_U8IN = U8 && (NA ? K == 1 : K == 0);   // aggregate reads the byte ring directly
@@ -938,7 +955,7 @@ struct Pipe {
     template <class Op>
     __device__ __forceinline__ void fused_run(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                               uint32_t nens, const Op op) {
-        if constexpr (!TAG) fused_full(in, imask, h, nens, op);
+        if constexpr (!TGE<AGE>) fused_full(in, imask, h, nens, op);
         else
             for (uint32_t k = 0; k < nens; ++k) {
                 if constexpr (AT::heavy)
@@ -981,7 +998,7 @@ struct Pipe {
     __device__ __forceinline__ void run_full(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                              uint32_t nens) {
         if constexpr (n == K + 1) {
-            if constexpr (!TAG) {
+            if constexpr (!TGE<K>) {
                 agg_full(in, imask, h, nens);
             } else {
                 for (uint32_t k = 0; k < nens; ++k) agg_tagged(in, tin, imask, h + k * W, W, OpAll{});
@@ -1078,14 +1095,14 @@ struct Pipe {
             // signals (credit 0, A4) are consumed in one pass; the first later
             // signal with a positive credit moves it into the counter (rule 2b)
             // so the next data phase starts without re-reading the queue.
-            if (TAG || !spend || E<ei>().cur != 0) {
+            if (TGE<ei> || !spend || E<ei>().cur != 0) {
                 if (!did) break;
                 prog = true;
                 continue;
             }
             uint32_t nsig = 0;
             for (;;) {
-                if constexpr (!AGGN) {
+                if constexpr (!AGGN && !TGE<n>) {
                     if (scap - (E<n>().st - E<n>().sh) == 0) break;   // output signal queue full
                 }
                 const uint2 hs = S<ei>()[E<ei>().sh & smask];
@@ -1108,6 +1125,8 @@ struct Pipe {
                         if (lane == 0) store_key(hs.x, v);
                         acc = AT::id();
                     }
+                } else if constexpr (TGE<n>) {
+                    if (!is_end) ckey = hs.x;    // hybrid converter: outputs carry this key as their tag
                 } else {
                     push_signal<n>(hs.x, is_end, E<n>().sent);   // forwarded with a fresh credit
                 }
@@ -1176,12 +1195,12 @@ struct Pipe {
             const uint32_t idx = j * 32 + lane;
             const bool act = idx < e;
             v[j] = act ? agg_load(in, h + idx, imask) : 0u;
-            tg[j] = (TAG && act) ? tin[(h + idx) & imask] : 0u;
+            tg[j] = (TGE<AGE> && act) ? tin[(h + idx) & imask] : 0u;
             bool keep = act && op(v[j]);
             px[j] = py[j] = 0u;
             if constexpr (PAIR) {
                 if (keep) {
-                    const uint32_t key = TAG ? tg[j] : ekey;
+                    const uint32_t key = TGE<AGE> ? tg[j] : ekey;
                     const uint32_t r = region_key(key);
                     keep = parse_pair(chunk_base(key) + (long long)(v[j] >> 8), P.off[r + 1], px[j], py[j]);
                 }
@@ -1194,7 +1213,7 @@ struct Pipe {
         if (lane == 0) base = atomicAdd(P.emit_n, (unsigned long long)total);
         base = __shfl_sync(kFull, base, 0);
         if (base + total > P.emit_cap && lane == 0) atomicCAS((int *)&P.hdr->err, 0, ERR_EMIT_FULL);
-        const uint32_t ureg = TAG ? 0u : region_key(ekey);
+        const uint32_t ureg = TGE<AGE> ? 0u : region_key(ekey);
         uint32_t rel = 0;
 #pragma unroll
         for (int j = 0; j < IPL; ++j) {
@@ -1207,7 +1226,7 @@ struct Pipe {
                     } else {
                         P.emit_vals[pos] = v[j];
                     }
-                    P.emit_regs[pos] = TAG ? region_key(tg[j]) : ureg;
+                    P.emit_regs[pos] = TGE<AGE> ? region_key(tg[j]) : ureg;
                 }
             }
             rel += __popc(mk[j]);
@@ -1546,9 +1565,9 @@ struct Pipe {
     __device__ __forceinline__ void run_partial(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                                 uint32_t e) {
         if constexpr (n == K + 1) {
-            if constexpr (!TAG && EMIT) {
+            if constexpr (!TGE<K> && EMIT) {
                 emit_ens(in, nullptr, imask, h, e, OpAll{});
-            } else if constexpr (!TAG) {
+            } else if constexpr (!TGE<K>) {
 #pragma unroll
                 for (int j = 0; j < IPL; ++j) {
                     const uint32_t idx = j * 32 + lane;
@@ -1558,9 +1577,9 @@ struct Pipe {
                 agg_tagged(in, tin, imask, h, e, OpAll{});
             }
         } else if constexpr (NA && n == K) {
-            if constexpr (!TAG && EMIT) {
+            if constexpr (!TGE<K - 1> && EMIT) {
                 with_op(P.st[n - 1], pvn(n), [&](auto op) { emit_ens(in, nullptr, imask, h, e, op); });
-            } else if constexpr (!TAG) {
+            } else if constexpr (!TGE<K - 1>) {
                 with_op(P.st[n - 1], pvn(n), [&](auto op) {
                     const FusedAcc<AT> r = fused_partial<AT, decltype(op), AGG_U8IN>(in, imask, h, e, op, adelta, P.C - 1,
                                                                                      FusedAcc<AT>{acc, fkept});
@@ -1573,9 +1592,10 @@ struct Pipe {
         } else {
             uint32_t tl = E<n>().qt;
             with_op(P.st[n - 1], pvn(n), [&](auto op) {
-                tl = partial_stage<TAG, decltype(op), U8 && n == 1>(op, in, tin, imask, h, e, Q<n>(), T<n>(), qm<n>(),
-                                                                    tl, lt, P.C - 1);
+                tl = partial_stage<TGE<n - 1>, decltype(op), U8 && n == 1>(op, in, tin, imask, h, e, Q<n>(), T<n>(),
+                                                                           qm<n>(), tl, lt, P.C - 1);
             });
+            if constexpr (HYB > 0 && n == HYB) stamp_tags<n>(E<n>().qt, tl);
             E<n>().sent += tl - E<n>().qt;
             E<n>().qt = tl;
         }
@@ -1676,7 +1696,7 @@ struct Pipe {
             const uint32_t shift = E<e - 1>().qh - E<e>().qt;
             if (shift != 0) {
                 const uint32_t n = E<e>().qt - E<e>().qh;
-                if (n != 0) move_items<TAG>(Q<0>(), T<0>(), E<e>().qt, n, shift, ring0 - 1);
+                if (n != 0) move_items<TAGANY>(Q<0>(), T<0>(), E<e>().qt, n, shift, ring0 - 1);
                 E<e>().qh += shift;
                 E<e>().qt += shift;
                 q_start[e] += shift;
@@ -1775,7 +1795,7 @@ struct Pipe {
                 break;
             }
         }
-        if constexpr (TAG) flush_tagged();
+        if constexpr (TGE<AGE>) flush_tagged();
         if constexpr (CTX) ctx_close(0xffffffffu);
         // drain outstanding TMA stages before the CTA's shared memory is released
         for (uint32_t spins = 0; landed_j < stg_j && spins < (1u << 26); ++spins) {
@@ -1793,12 +1813,12 @@ struct Pipe {
     }
 };
 
-template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false>
+template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false, int HYB = 0>
 __global__ void __launch_bounds__(WPB_MAX * 32, 1) k_pipeline(const __grid_constant__ KParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    using PP = Pipe<K, AGG, TAG, FUSE, CTX, TR>;
+    using PP = Pipe<K, AGG, TAG, FUSE, CTX, TR, HYB>;
     uint8_t *mine = smem + (size_t)warp * PP::smem_bytes(P.qcap, P.scap, P.ring0);
     if (P.hdr->err) return;
     if (P.auto_sel && P.hdr->sel != P.auto_sel - 1) return;   // AUTO: the other strategy's kernel runs

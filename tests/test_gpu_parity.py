@@ -553,3 +553,64 @@ def test_taxi_two_stage(rs, strategy, mode, stage1):
     got = got[np.lexsort((got[:, 2], got[:, 1], got[:, 0]))]
     ref = exp[np.lexsort((exp[:, 2], exp[:, 1], exp[:, 0]))]
     np.testing.assert_array_equal(got, ref)
+
+
+@pytest.mark.parametrize("nst,tag_from,mode", [(1, 1, "unfused"), (2, 1, "seq"), (3, 1, "seq"), (3, 2, "seq"),
+                                              (3, 3, "unfused"), (4, 2, "unfused"), (4, 3, "seq")])
+def test_hybrid_per_stage(rs, nst, tag_from, mode):
+    """RS_STRATEGY_HYBRID: signals up to
+    edge tag_from, tags after it.  Bit-identical integer aggregates with the
+    oracle over short, long, empty and chunk-spanning regions; the stages
+    before the converter keep the signal strategy's ensembles (bounded by
+    regions) and the stages after it run full ensembles like the tagged one."""
+    for L, dist in ((40, "var"), (700, "fixed"), (3000, "var")):
+        lens = synth.lengths(max(8, (1 << 17) // L), dist, L=L, seed=L + nst)
+        off = synth.offsets(lens, base=2)
+        vals = synth.values(int(off[-1]) + 5, "i32", seed=L + 1)
+        stages = synth.sweep_stages(nst)
+        ref = oracle.brute(vals, off, stages, "sum_i64")
+        got, st, _ = run_gpu(rs, vals, off, stages, "sum_i64", "hybrid", mode, tag_from=tag_from, chunk=2048,
+                             queue_cap=1024 if L == 40 else 0)
+        assert_parity(got, ref, "sum_i64")
+        kc = oracle.node_counts(vals, off, stages)
+        assert st[0][2] == off[-1] - off[0]
+        for j in range(nst + (1 if mode == "unfused" else 0)):
+            assert st[j + 1][2] == kc[:, j].sum()
+        if L == 40:
+            # after the converter, ensembles are full except at chunk / stream tails
+            n_after = tag_from + 1
+            if n_after <= nst or mode == "unfused":
+                d, f = st[n_after][0], st[n_after][1]
+                assert f >= 0.8 * d, (n_after, st[n_after])
+    with pytest.raises(rs.RSError):
+        rs.Pipeline(synth.sweep_stages(2), "sum_i64", strategy="hybrid", tag_from=2)   # fused: tag_from <= 1
+
+
+@pytest.mark.parametrize("mode", ["unfused"])
+def test_taxi_hybrid(rs, mode):
+    """The paper's best taxi variant: stage 1 (the '{' filter)
+    runs signal-delimited, stage 2 (parse + emit) runs on tagged items."""
+    b, off, exp = synth.taxi(600, seed=23)
+    p = rs.Pipeline(synth.taxi_stages(), "emit_pair", strategy="hybrid", tag_from=1,
+                    flags=rs.RS_FLAG_STATS | rs.RS_FLAG_UNFUSED, chunk=2048, grid=1)   # one instance: no early drain
+    e = torch.from_numpy(b).cuda()
+    o = torch.from_numpy(off).cuda()
+    R = off.size - 1
+    cap = exp.shape[0] + 8
+    v = torch.empty(2 * cap, dtype=torch.int32, device="cuda")
+    rg = torch.empty(cap, dtype=torch.int32, device="cuda")
+    cnt = torch.empty(1, dtype=torch.int64, device="cuda")
+    ws = p.alloc_workspace(R, e.numel())
+    p.run_emit(e, o, v, rg, cnt, ws)
+    torch.cuda.synchronize()
+    assert p.check() == 0
+    n = int(cnt.item())
+    assert n == exp.shape[0]
+    vv = v[:2 * n].cpu().numpy().view(np.uint32).reshape(n, 2)
+    got = np.stack([rg[:n].cpu().numpy().view(np.uint32), vv[:, 0], vv[:, 1]], 1)
+    got = got[np.lexsort((got[:, 2], got[:, 1], got[:, 0]))]
+    ref = exp[np.lexsort((exp[:, 2], exp[:, 1], exp[:, 0]))]
+    np.testing.assert_array_equal(got, ref)
+    st = p.stats()
+    assert st[2][1] >= 0.9 * st[2][0]          # stage 2 on tagged items: full ensembles
+    assert st[1][1] >= 0.8 * st[1][0]          # stage 1 (long lines, signal-delimited): mostly full (P:684-686: 91%)
