@@ -567,7 +567,7 @@ def run_ours(args):
         del vals, off, out, ws
         torch.cuda.empty_cache()
         sweep = run_sweep(rs, torch, dev, args)
-        configs = run_configs(rs, torch, dev, args)
+        configs = run_configs(rs, torch, dev, args) + run_taxi(rs, torch, dev, args)
 
     occ = lane_stats(st)
     if occ_bound is not None:
@@ -600,6 +600,47 @@ def run_ours(args):
     if configs is not None:
         line["configs"] = configs
     print(json.dumps(line), flush=True)
+
+
+def run_taxi(rs, torch, dev, args, reps=2):
+    """The taxi-style two-stage app: lines of text
+    with "{x,y}" pairs; stage 1 keeps the '{' bytes, stage 2 parses, verifies,
+    swaps and emits (line, y, x).  Like the paper's replicated DIBS file
+    (P:698-705), a 2000-line synthetic corpus is replicated to ~2^28 bytes.
+    Signal, tagged and the paper's mix (signal stage 1, tags in stage 2:
+    hybrid tag_from=1), each with stage 2 as its own node (unfused)."""
+    import synth
+    b, off, exp = synth.taxi(2000, seed=5)
+    rep = max(1, (1 << 28) // b.size)
+    bt = torch.from_numpy(b).to(dev).repeat(rep)
+    o1 = torch.from_numpy(off).to(dev)
+    offs = torch.cat([o1[:-1] + k * b.size for k in range(rep)] + [torch.tensor([rep * b.size], device=dev)])
+    R = offs.numel() - 1
+    n = int(bt.numel())
+    cap = exp.shape[0] * rep + 64
+    res = []
+    for strat, kw in (("signal", {}), ("tagged", {}), ("hybrid", {"tag_from": 1})):
+        p = rs.Pipeline(synth.taxi_stages(), "emit_pair", strategy=strat,
+                        flags=rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING | rs.RS_FLAG_UNFUSED, **kw)
+        v = torch.empty(2 * cap, dtype=torch.int32, device=dev)
+        rg = torch.empty(cap, dtype=torch.int32, device=dev)
+        cnt = torch.empty(1, dtype=torch.int64, device=dev)
+        ws = p.alloc_workspace(R, n, dev)
+        p.run_emit(bt, offs, v, rg, cnt, ws)
+        torch.cuda.synchronize()
+        ms = []
+        for _ in range(reps):
+            p.run_emit(bt, offs, v, rg, cnt, ws)
+            ms.append(sum(p.kernel_times()))
+        t = statistics.median(ms)
+        occ = lane_stats(p.stats())
+        res.append({"workload": "taxi", "strategy": strat + ("(tag_from=1)" if kw else ""), "children": n,
+                    "regions": R, "pairs": int(cnt.item()), "pairs_expected": int(exp.shape[0] * rep),
+                    "ms": t, "items_per_s": n / (t / 1e3),
+                    "full_rate": [x["full_rate"] for x in occ], "lane_fraction": [x["lane_fraction"] for x in occ],
+                    "error": p.check()})
+        del p, v, rg, ws
+    return res
 
 
 def run_configs(rs, torch, dev, args):
