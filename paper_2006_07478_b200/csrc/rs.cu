@@ -278,7 +278,7 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     if (cfg.signal_cap == 0)
         cfg.signal_cap = inplace ? 32 : (nst_ >= 2 ? 64 : 128);   // (context strategy: profiles/r1_tuning.txt)
     if (cfg.q0_stage == 0)
-        cfg.q0_stage = inplace ? (tagged_ ? 512 : 1024) : ((tagged_ || nst_ >= 2) ? 256 : 512);
+        cfg.q0_stage = inplace ? (tagged_ ? 512 : 1024) : ((tagged_ || nst_ >= 2) ? 256 : 2048);   // byte streams: SWAR wants big stages
     if (!is_pow2(cfg.queue_cap) || cfg.queue_cap < 2 * W || cfg.queue_cap > 65536)
         return fail(RS_ERR_UNSUPPORTED, "queue_cap must be a power of 2 in [256, 65536]");
     if (!is_pow2(cfg.signal_cap) || cfg.signal_cap < 4 || cfg.signal_cap > 65536)
@@ -320,10 +320,17 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
                     }
                     p->has_parent = true;
                     break;
-                case RS_OP_CLASS:
+                case RS_OP_CLASS: {
                     if (!nd.table) { delete p; return fail(RS_ERR_INVALID_ARG, "CLASS needs a 32-byte table"); }
                     if (elem != RS_U8) { delete p; return fail(RS_ERR_UNSUPPORTED, "CLASS needs u8 elements"); }
-                    std::memcpy(s.table, nd.table, 32); break;
+                    std::memcpy(s.table, nd.table, 32);
+                    // a single-member class runs the SWAR byte test (a = 0x100 | member)
+                    int members = 0, last = 0;
+                    for (int c = 0; c < 256; ++c)
+                        if ((nd.table[c >> 3] >> (c & 7)) & 1) { ++members; last = c; }
+                    if (members == 1) s.a = 0x100u | (uint32_t)last;
+                    break;
+                }
                 default: delete p; return fail(RS_ERR_UNSUPPORTED, "unknown FILTER op");
             }
         } else {

@@ -5,6 +5,7 @@
 // signal queue.  See rs.cu's header comment for the model; the
 // citations below point at the PAPER.md lines each step realises.
 #pragma once
+#include <type_traits>
 
 // ------------------------------------------------- filter / transform ops
 // isGood() / push() bodies (Fig. 5), specialised per op so the
@@ -24,6 +25,18 @@ struct OpLt {
 struct OpClass {
     const uint32_t *tbl;
     __device__ __forceinline__ bool operator()(uint32_t &v) const { return (tbl[(v & 0xffu) >> 5] >> (v & 31u)) & 1u; }
+};
+// CLASS with a single member byte c (the text config's '{'): the scalar form
+// for the generic paths, and match4() -- a SWAR test of four bytes at once
+// (exact zero-byte detection of w ^ c4, no carries across bytes): 0x80 in
+// every byte of w that equals c.
+struct OpClass1 {
+    uint32_t c4;           // c replicated into the four bytes
+    __device__ __forceinline__ bool operator()(uint32_t &v) const { return (v & 0xffu) == (c4 & 0xffu); }
+    __device__ __forceinline__ uint32_t match4(uint32_t w) const {
+        const uint32_t x = w ^ c4;
+        return ~(((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x) & 0x80808080u;
+    }
 };
 struct OpScale {
     float s;
@@ -110,11 +123,49 @@ __device__ __forceinline__ void filter_slices(const uint32_t *in, const uint32_t
     tl += all;
 }
 
+// SWAR filter ensemble over a byte ring, single-member CLASS:
+// the e <= w bytes at h are read one 32-bit word per lane (lane l: bytes
+// 4l .. 4l+3, a funnel shift realigns an unaligned head) and tested four at a
+// time (OpClass1::match4); the sparse survivors are compacted in stream
+// order -- lane l's survivors follow those of lanes < l, found from three
+// ballots of its survivor count (0..4) -- as items byte | (pos mod C) << 8
+// into the 4-byte output queue.  Returns the new output tail.
+__device__ __forceinline__ uint32_t swar_filter(const uint32_t *in, uint32_t imask, uint32_t h, uint32_t e,
+                                                uint32_t *out, uint32_t qmask, uint32_t tl, const OpClass1 &op,
+                                                uint32_t lt, uint32_t cmask) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t wmask = imask >> 2;
+    const uint32_t a = h & 3u;
+    const uint32_t wi = ((h >> 2) + lane) & wmask;
+    uint32_t w = in[wi];
+    if (a) w = __funnelshift_r(w, in[(wi + 1) & wmask], 8u * a);
+    uint32_t m = op.match4(w);
+    if (e < (uint32_t)W) {
+        const int valid = (int)e - 4 * (int)lane;
+        m &= valid >= 4 ? 0xffffffffu : (valid <= 0 ? 0u : (0xffffffffu >> (32 - 8 * valid)));
+    }
+    const uint32_t c = __popc(m);
+    const uint32_t b0 = __ballot_sync(kFull, c & 1u), b1 = __ballot_sync(kFull, c & 2u), b2 = __ballot_sync(kFull, c & 4u);
+    uint32_t at = tl + __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
+    while (m) {
+        const uint32_t k = (__ffs(m) - 1) >> 3;
+        m &= m - 1u;
+        const uint32_t pos = h + 4u * lane + k;
+        out[at & qmask] = ((w >> (8u * k)) & 0xffu) | ((pos & cmask) << 8);
+        ++at;
+    }
+    return tl + __popc(b0) + 2u * __popc(b1) + 4u * __popc(b2);
+}
+
 template <bool TAG, class Op, bool U8IN = false>
 __device__ __noinline__ uint32_t filter_batch(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                               uint32_t nens, uint32_t *out, uint32_t *tout, uint32_t qmask,
                                               uint32_t tl, const Op op, uint32_t lt, uint32_t cmask = 0) {
-    for (uint32_t k = 0; k < nens; ++k, h += W) filter_slices<TAG, IPL, Op, U8IN>(in, tin, imask, h, out, tout, qmask, tl, op, lt, cmask);
+    if constexpr (!TAG && U8IN && std::is_same<Op, OpClass1>::value) {
+        for (uint32_t k = 0; k < nens; ++k, h += W) tl = swar_filter(in, imask, h, W, out, qmask, tl, op, lt, cmask);
+    } else {
+        for (uint32_t k = 0; k < nens; ++k, h += W) filter_slices<TAG, IPL, Op, U8IN>(in, tin, imask, h, out, tout, qmask, tl, op, lt, cmask);
+    }
     __syncwarp();
     return tl;
 }
@@ -127,6 +178,11 @@ template <bool TAG, class Op, bool U8IN>
 __device__ __noinline__ uint32_t partial_stage(const Op op, const uint32_t *in, const uint32_t *tin,
                                                uint32_t imask, uint32_t h, uint32_t e, uint32_t *out, uint32_t *tout,
                                                uint32_t qmask, uint32_t tl, uint32_t lt, uint32_t cmask) {
+    if constexpr (!TAG && U8IN && std::is_same<Op, OpClass1>::value) {
+        tl = swar_filter(in, imask, h, e, out, qmask, tl, op, lt, cmask);
+        __syncwarp();
+        return tl;
+    }
     const uint32_t lane = threadIdx.x & 31u;
     uint32_t v[IPL], tg[IPL];
 #pragma unroll
@@ -167,7 +223,10 @@ __device__ __forceinline__ void with_op(const StageP &sp, uint32_t pv, F &&f) {
             if (sp.table[0]) f(OpAll{});
             else f(OpLt{sp.b, false});
             break;
-        case RS_OP_CLASS: f(OpClass{sp.table}); break;
+        case RS_OP_CLASS:
+            if (sp.a & 0x100u) f(OpClass1{(sp.a & 0xffu) * 0x01010101u});
+            else f(OpClass{sp.table});
+            break;
         case RS_OP_SCALE_F32: f(OpScale{__uint_as_float(sp.a)}); break;
         default: f(OpAffine{sp.a, sp.b}); break;
     }
@@ -914,12 +973,51 @@ struct Pipe {
         if (k < nens) agg_slices<IPL>(in, imask, h);
     }
 
+    // Text (byte stream), single-stage fused CLASS + aggregate, single-member
+    // class (SWAR): an ensemble of w = 128 bytes is read as one
+    // 32-bit word per lane (lane l holds bytes 4l .. 4l+3; a funnel shift
+    // realigns an unaligned head), tested four bytes at a time (match4), and
+    // only the sparse survivors are lifted (the hash of their index within
+    // the line) -- instead of a byte load, a table lookup and a select per
+    // byte.  e < w: a partial ensemble (bytes 4l + k >= e masked off).  The
+    // fold is commutative, so the lane-major item order does not matter.
+    __device__ __forceinline__ void swar_ens(const uint32_t *in, uint32_t imask, uint32_t h, uint32_t e,
+                                             const OpClass1 &op) {
+        const uint32_t *wring = in;                      // the byte ring as words (size a multiple of 16 bytes)
+        const uint32_t wmask = imask >> 2;
+        const uint32_t a = h & 3u;
+        const uint32_t wi = ((h >> 2) + lane) & wmask;
+        uint32_t w = wring[wi];
+        if (a) w = __funnelshift_r(w, wring[(wi + 1) & wmask], 8u * a);
+        uint32_t m = op.match4(w);
+        if (e < (uint32_t)W) {
+            const int valid = (int)e - 4 * lane;         // bytes of this lane inside the ensemble
+            m &= valid >= 4 ? 0xffffffffu : (valid <= 0 ? 0u : (0xffffffffu >> (32 - 8 * valid)));
+        }
+        fkept += __popc(m);
+        const uint32_t cm = P.C - 1;
+        while (__any_sync(kFull, m != 0)) {
+            if (m) {
+                const uint32_t bit = __ffs(m) - 1;       // 8k + 7 for byte k
+                m &= m - 1u;
+                const uint32_t k = bit >> 3;
+                const uint32_t pos = h + 4u * lane + k;
+                const uint32_t v = ((w >> (8u * k)) & 0xffu) | ((pos & cm) << 8);
+                acc = AT::comb(acc, AT::lift_i(v, adelta));
+            }
+        }
+    }
+
     // Fused node K, full ensembles (signal strategy): apply the op, fold the
     // survivors into the per-lane accumulator (isGood + a::run).
     template <class Op>
     __device__ __forceinline__ void fused_full(const uint32_t *in, uint32_t imask, uint32_t h, uint32_t nens, const Op op) {
         if constexpr (EMIT) {
             for (uint32_t k = 0; k < nens; ++k) emit_ens(in, nullptr, imask, h + k * W, W, op);
+            return;
+        }
+        if constexpr (K == 1 && AGG_U8IN && AT::heavy && std::is_same<Op, OpClass1>::value) {
+            for (uint32_t k = 0; k < nens; ++k, h += W) swar_ens(in, imask, h, W, op);
             return;
         }
         if constexpr (K == 1) {
@@ -1014,7 +1112,10 @@ struct Pipe {
                     if (sp.table[0]) fused_run(in, tin, imask, h, nens, OpAll{});
                     else fused_run(in, tin, imask, h, nens, OpLt{sp.b, false});
                     break;
-                case RS_OP_CLASS: fused_run(in, tin, imask, h, nens, OpClass{sp.table}); break;
+                case RS_OP_CLASS:
+                    if (sp.a & 0x100u) fused_run(in, tin, imask, h, nens, OpClass1{(sp.a & 0xffu) * 0x01010101u});
+                    else fused_run(in, tin, imask, h, nens, OpClass{sp.table});
+                    break;
                 case RS_OP_PARENT_LT: fused_run(in, tin, imask, h, nens, OpLt{pvn(n), false}); break;
                 case RS_OP_SCALE_F32: fused_run(in, tin, imask, h, nens, OpScale{__uint_as_float(sp.a)}); break;
                 default: fused_run(in, tin, imask, h, nens, OpAffine{sp.a, sp.b}); break;
@@ -1030,7 +1131,10 @@ struct Pipe {
                     if (sp.table[0]) filter_full<n>(in, tin, imask, h, nens, OpAll{});
                     else filter_full<n>(in, tin, imask, h, nens, OpLt{sp.b, false});
                     break;
-                case RS_OP_CLASS: filter_full<n>(in, tin, imask, h, nens, OpClass{sp.table}); break;
+                case RS_OP_CLASS:
+                    if (sp.a & 0x100u) filter_full<n>(in, tin, imask, h, nens, OpClass1{(sp.a & 0xffu) * 0x01010101u});
+                    else filter_full<n>(in, tin, imask, h, nens, OpClass{sp.table});
+                    break;
                 case RS_OP_PARENT_LT: filter_full<n>(in, tin, imask, h, nens, OpLt{pvn(n), false}); break;
                 case RS_OP_SCALE_F32: filter_full<n>(in, tin, imask, h, nens, OpScale{__uint_as_float(sp.a)}); break;
                 default: filter_full<n>(in, tin, imask, h, nens, OpAffine{sp.a, sp.b}); break;
@@ -1581,6 +1685,10 @@ struct Pipe {
                 with_op(P.st[n - 1], pvn(n), [&](auto op) { emit_ens(in, nullptr, imask, h, e, op); });
             } else if constexpr (!TGE<K - 1>) {
                 with_op(P.st[n - 1], pvn(n), [&](auto op) {
+                    if constexpr (K == 1 && AGG_U8IN && AT::heavy && std::is_same<decltype(op), OpClass1>::value) {
+                        swar_ens(in, imask, h, e, op);
+                        return;
+                    }
                     const FusedAcc<AT> r = fused_partial<AT, decltype(op), AGG_U8IN>(in, imask, h, e, op, adelta, P.C - 1,
                                                                                      FusedAcc<AT>{acc, fkept});
                     acc = r.acc;

@@ -20,6 +20,7 @@ ap.add_argument("--workload", default="sweep_fixed_L4096")
 ap.add_argument("--strategy", default="signal")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--profile", action="store_true")
+ap.add_argument("--flags", type=int, default=0)
 ap.add_argument("cfgs", nargs="*")
 a = ap.parse_args()
 spec = bench.workload_spec(a.workload)
@@ -31,7 +32,7 @@ for c in (a.cfgs or ["0:0:0"]):
     q, s, sc = (int(x) for x in c.split(":"))
     try:
         p = rs.Pipeline(spec["stages"], spec["agg"], strategy=a.strategy, queue_cap=q, q0_stage=s, signal_cap=sc,
-                        flags=rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING)
+                        flags=rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING | a.flags)
         out = p.alloc_outputs(R, dev)
         ws = p.alloc_workspace(R, vals.numel(), dev)
         for _ in range(3):
