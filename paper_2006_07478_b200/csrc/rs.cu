@@ -298,6 +298,18 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     p->agg = agg;
     for (int i = 0; i < nst; ++i) {
         const rs_node &nd = nodes[i + 1];
+        // op sets per element type (the kernels compile only these, rs_pipe.cuh with_op_k)
+        const bool ok = elem == RS_U8 ? nd.op == RS_OP_CLASS
+                      : elem == RS_F32 ? (nd.op == RS_OP_HASH_LT || nd.op == RS_OP_LT_U32 || nd.op == RS_OP_SCALE_F32 ||
+                                          nd.op == RS_OP_PARENT_LT)
+                                       : (nd.op == RS_OP_HASH_LT || nd.op == RS_OP_LT_U32 || nd.op == RS_OP_AFFINE_I32 ||
+                                          nd.op == RS_OP_PARENT_LT);
+        if (!ok) {
+            delete p;
+            return fail(RS_ERR_UNSUPPORTED, "op " + std::to_string(nd.op) + " is not built for this element type "
+                                            "(i32/u32: HASH_LT LT_U32 AFFINE_I32 PARENT_LT; f32: HASH_LT LT_U32 "
+                                            "SCALE_F32 PARENT_LT; u8: CLASS)");
+        }
         StageP &s = p->st[i];
         std::memset(&s, 0, sizeof s);
         s.kind = nd.kind;

@@ -209,29 +209,6 @@ __device__ __noinline__ uint32_t partial_stage(const Op op, const uint32_t *in, 
     return tl;
 }
 
-// Calls f(op) with the node's op as its specialised functor (one switch per
-// firing instead of one per item).
-template <class F>
-__device__ __forceinline__ void with_op(const StageP &sp, uint32_t pv, F &&f) {
-    switch (sp.op) {
-        case RS_OP_PARENT_LT: f(OpLt{pv, false}); break;   // pv = the open region's context (getParent)
-        case RS_OP_HASH_LT:
-            if (sp.b >= 256) f(OpAll{});
-            else f(OpHash{sp.a, sp.b << 24});
-            break;
-        case RS_OP_LT_U32:
-            if (sp.table[0]) f(OpAll{});
-            else f(OpLt{sp.b, false});
-            break;
-        case RS_OP_CLASS:
-            if (sp.a & 0x100u) f(OpClass1{(sp.a & 0xffu) * 0x01010101u});
-            else f(OpClass{sp.table});
-            break;
-        case RS_OP_SCALE_F32: f(OpScale{__uint_as_float(sp.a)}); break;
-        default: f(OpAffine{sp.a, sp.b}); break;
-    }
-}
-
 // Fused terminal node, full ensembles, signal strategy (see Pipe::FUSE): the
 // node's op decides each item, survivors are folded into the per-lane
 // accumulator (isGood + a::run).  Out of line so the hot loop
@@ -383,6 +360,20 @@ struct Chunk {
 // (survivors before it), and the aggregate gives each lane the key of the last
 // boundary at or before its item -- the context computed per lane instead of
 // stored with the items.
+// PARENT_LT, out of line (rare: once per region per parent-context node, and
+// only in pipelines that have one): *dst = ctx[region of key]; SLOT keys name
+// the region split across chunk k's boundary (see Pipe::region_key).
+static __device__ __noinline__ void load_pv(const uint32_t *ctx, const uint32_t *chunk_fr, uint32_t key, uint32_t *dst) {
+    uint32_t r = key;
+    if (key & SLOT) {
+        const uint32_t slot = key & ~SLOT, k = slot >> 1;
+        r = ((slot & 1u) ? chunk_fr[k + 1] : chunk_fr[k]) - 1u;
+    }
+    const uint32_t v = ctx[r];
+    if ((threadIdx.x & 31u) == 0) *dst = v;
+    __syncwarp();
+}
+
 template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false, int HYB = 0>
 struct Pipe {
     using AT = AggT<AGG>;
@@ -416,9 +407,12 @@ struct Pipe {
     // per-instance shared header: [0,64) TMA barriers, [64,160) node counters
     // (u32 x 24: data firings, full firings, items, signals per node),
     // [160,288) RS_FLAG_PROFILE cycle counters (u64 x 16)
-    // [288, 320) parent-context value of the open region per node (PARENT_LT)
-    static constexpr uint32_t HDR = CTX ? 448 : 320;     // CTX: + 32-word key scratch at [320, 448)
-    static constexpr uint32_t CNT_OFF = 64, PROF_OFF = 160, PV_OFF = 288, SCR_OFF = 320;
+    // parent-context value of the open region per node (PARENT_LT): in the
+    // profile area [160, 288) of the production kernels (no profiling code),
+    // after it in the debug (TR) ones
+    static constexpr uint32_t BASE_HDR = TR ? 320 : 288;
+    static constexpr uint32_t HDR = CTX ? BASE_HDR + 128 : BASE_HDR;   // CTX: + 32-word key scratch
+    static constexpr uint32_t CNT_OFF = 64, PROF_OFF = 160, PV_OFF = TR ? 288 : 160, SCR_OFF = BASE_HDR;
 
     const KParams &P;
     const int lane;
@@ -693,9 +687,7 @@ struct Pipe {
         return ((slot & 1u) ? P.chunk_fr[k + 1] : P.chunk_fr[k]) - 1u;
     }
     __device__ __forceinline__ void set_pv(int n, uint32_t key) const {
-        const uint32_t v = P.ctx[region_key(key)];
-        if (lane == 0) reinterpret_cast<uint32_t *>(base + PV_OFF)[n] = v;
-        __syncwarp();
+        load_pv(P.ctx, P.chunk_fr, key, reinterpret_cast<uint32_t *>(base + PV_OFF) + n);
     }
     __device__ __forceinline__ uint32_t pvn(int n) const { return reinterpret_cast<const uint32_t *>(base + PV_OFF)[n]; }
 
@@ -1102,44 +1094,40 @@ struct Pipe {
                 for (uint32_t k = 0; k < nens; ++k) agg_tagged(in, tin, imask, h + k * W, W, OpAll{});
             }
         } else if constexpr (NA && n == K) {
-            const StageP &sp = P.st[n - 1];
-            switch (sp.op) {
-                case RS_OP_HASH_LT:
-                    if (sp.b >= 256) fused_run(in, tin, imask, h, nens, OpAll{});
-                    else fused_run(in, tin, imask, h, nens, OpHash{sp.a, sp.b << 24});
-                    break;
-                case RS_OP_LT_U32:
-                    if (sp.table[0]) fused_run(in, tin, imask, h, nens, OpAll{});
-                    else fused_run(in, tin, imask, h, nens, OpLt{sp.b, false});
-                    break;
-                case RS_OP_CLASS:
-                    if (sp.a & 0x100u) fused_run(in, tin, imask, h, nens, OpClass1{(sp.a & 0xffu) * 0x01010101u});
-                    else fused_run(in, tin, imask, h, nens, OpClass{sp.table});
-                    break;
-                case RS_OP_PARENT_LT: fused_run(in, tin, imask, h, nens, OpLt{pvn(n), false}); break;
-                case RS_OP_SCALE_F32: fused_run(in, tin, imask, h, nens, OpScale{__uint_as_float(sp.a)}); break;
-                default: fused_run(in, tin, imask, h, nens, OpAffine{sp.a, sp.b}); break;
-            }
+            with_op_k(P.st[n - 1], pvn(n), [&](auto op) { fused_run(in, tin, imask, h, nens, op); });
         } else {
-            const StageP &sp = P.st[n - 1];
+            with_op_k(P.st[n - 1], pvn(n), [&](auto op) { filter_full<n>(in, tin, imask, h, nens, op); });
+            __syncwarp();
+        }
+    }
+
+    // Calls f(op) with stage sp's op as its specialised functor -- one switch
+    // per firing, not per item.  Only the ops the host accepts for this
+    // kernel's element type are compiled in (i32/u32: HASH_LT, LT_U32,
+    // AFFINE_I32, PARENT_LT; f32: HASH_LT, LT_U32, SCALE_F32, PARENT_LT;
+    // u8: CLASS): unused op code would only dilute the instruction cache.
+    static constexpr bool EU8 = U8, EF32 = (AGG == 21);
+    template <class F>
+    __device__ __forceinline__ void with_op_k(const StageP &sp, uint32_t pv, F &&f) const {
+        if constexpr (EU8) {
+            if (sp.a & 0x100u) f(OpClass1{(sp.a & 0xffu) * 0x01010101u});
+            else f(OpClass{sp.table});
+        } else {
             switch (sp.op) {
+                case RS_OP_PARENT_LT: f(OpLt{pv, false}); break;   // pv = the open region's context (getParent)
                 case RS_OP_HASH_LT:
-                    if (sp.b >= 256) filter_full<n>(in, tin, imask, h, nens, OpAll{});
-                    else filter_full<n>(in, tin, imask, h, nens, OpHash{sp.a, sp.b << 24});
+                    if (sp.b >= 256) f(OpAll{});
+                    else f(OpHash{sp.a, sp.b << 24});
                     break;
                 case RS_OP_LT_U32:
-                    if (sp.table[0]) filter_full<n>(in, tin, imask, h, nens, OpAll{});
-                    else filter_full<n>(in, tin, imask, h, nens, OpLt{sp.b, false});
+                    if (sp.table[0]) f(OpAll{});
+                    else f(OpLt{sp.b, false});
                     break;
-                case RS_OP_CLASS:
-                    if (sp.a & 0x100u) filter_full<n>(in, tin, imask, h, nens, OpClass1{(sp.a & 0xffu) * 0x01010101u});
-                    else filter_full<n>(in, tin, imask, h, nens, OpClass{sp.table});
+                default:
+                    if constexpr (EF32) f(OpScale{__uint_as_float(sp.a)});
+                    else f(OpAffine{sp.a, sp.b});
                     break;
-                case RS_OP_PARENT_LT: filter_full<n>(in, tin, imask, h, nens, OpLt{pvn(n), false}); break;
-                case RS_OP_SCALE_F32: filter_full<n>(in, tin, imask, h, nens, OpScale{__uint_as_float(sp.a)}); break;
-                default: filter_full<n>(in, tin, imask, h, nens, OpAffine{sp.a, sp.b}); break;
             }
-            __syncwarp();
         }
     }
 
@@ -1448,9 +1436,9 @@ struct Pipe {
             uint32_t done = e;
             if constexpr (AGGN) {
                 if constexpr (n == K + 1) ctx_agg_ens(in, imask, E<ei>().qh, e, cons, OpAll{});
-                else with_op(P.st[n - 1], 0u, [&](auto op) { ctx_agg_ens(in, imask, E<ei>().qh, e, cons, op); });
+                else with_op_k(P.st[n - 1], 0u, [&](auto op) { ctx_agg_ens(in, imask, E<ei>().qh, e, cons, op); });
             } else {
-                with_op(P.st[n - 1], 0u, [&](auto op) { done = ctx_filter_ens<n>(in, imask, E<ei>().qh, e, cons, op); });
+                with_op_k(P.st[n - 1], 0u, [&](auto op) { done = ctx_filter_ens<n>(in, imask, E<ei>().qh, e, cons, op); });
             }
             if (done == 0) break;
             E<ei>().qh += done;
@@ -1682,9 +1670,9 @@ struct Pipe {
             }
         } else if constexpr (NA && n == K) {
             if constexpr (!TGE<K - 1> && EMIT) {
-                with_op(P.st[n - 1], pvn(n), [&](auto op) { emit_ens(in, nullptr, imask, h, e, op); });
+                with_op_k(P.st[n - 1], pvn(n), [&](auto op) { emit_ens(in, nullptr, imask, h, e, op); });
             } else if constexpr (!TGE<K - 1>) {
-                with_op(P.st[n - 1], pvn(n), [&](auto op) {
+                with_op_k(P.st[n - 1], pvn(n), [&](auto op) {
                     if constexpr (K == 1 && AGG_U8IN && AT::heavy && std::is_same<decltype(op), OpClass1>::value) {
                         swar_ens(in, imask, h, e, op);
                         return;
@@ -1699,7 +1687,7 @@ struct Pipe {
             }
         } else {
             uint32_t tl = E<n>().qt;
-            with_op(P.st[n - 1], pvn(n), [&](auto op) {
+            with_op_k(P.st[n - 1], pvn(n), [&](auto op) {
                 tl = partial_stage<TGE<n - 1>, decltype(op), U8 && n == 1>(op, in, tin, imask, h, e, Q<n>(), T<n>(),
                                                                            qm<n>(), tl, lt, P.C - 1);
             });
