@@ -312,25 +312,27 @@ KernelFn pick_k(int K) {
     }
 }
 
-template <int AGG, bool TAG, bool FUSE, bool CTX = false>
+template <int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false>
 uint32_t ring_for(int K, uint32_t sblk, uint32_t qcap) {
     switch (K) {
-        case 0: return Pipe<0, AGG, TAG, false, CTX>::ring_for(sblk, qcap);
-        case 1: return Pipe<1, AGG, TAG, FUSE, CTX>::ring_for(sblk, qcap);
-        case 2: return Pipe<2, AGG, TAG, FUSE, CTX>::ring_for(sblk, qcap);
-        case 3: return Pipe<3, AGG, TAG, FUSE, CTX>::ring_for(sblk, qcap);
-        default: return Pipe<4, AGG, TAG, FUSE, CTX>::ring_for(sblk, qcap);
+        case 0: return Pipe<0, AGG, TAG, false, CTX, TR>::ring_for(sblk, qcap);
+        case 1: return Pipe<1, AGG, TAG, FUSE, CTX, TR>::ring_for(sblk, qcap);
+        case 2: return Pipe<2, AGG, TAG, FUSE, CTX, TR>::ring_for(sblk, qcap);
+        case 3: return Pipe<3, AGG, TAG, FUSE, CTX, TR>::ring_for(sblk, qcap);
+        default: return Pipe<4, AGG, TAG, FUSE, CTX, TR>::ring_for(sblk, qcap);
     }
 }
 
-template <int AGG, bool TAG, bool FUSE, bool CTX = false>
+// shared memory of one instance (the kernel's per-warp window; it must be the
+// same instantiation as the kernel launched: the debug kernels' header differs)
+template <int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false>
 uint32_t smem_for(int K, uint32_t qcap, uint32_t scap, uint32_t ring) {
     switch (K) {
-        case 0: return Pipe<0, AGG, TAG, false, CTX>::smem_bytes(qcap, scap, ring);
-        case 1: return Pipe<1, AGG, TAG, FUSE, CTX>::smem_bytes(qcap, scap, ring);
-        case 2: return Pipe<2, AGG, TAG, FUSE, CTX>::smem_bytes(qcap, scap, ring);
-        case 3: return Pipe<3, AGG, TAG, FUSE, CTX>::smem_bytes(qcap, scap, ring);
-        default: return Pipe<4, AGG, TAG, FUSE, CTX>::smem_bytes(qcap, scap, ring);
+        case 0: return Pipe<0, AGG, TAG, false, CTX, TR>::smem_bytes(qcap, scap, ring);
+        case 1: return Pipe<1, AGG, TAG, FUSE, CTX, TR>::smem_bytes(qcap, scap, ring);
+        case 2: return Pipe<2, AGG, TAG, FUSE, CTX, TR>::smem_bytes(qcap, scap, ring);
+        case 3: return Pipe<3, AGG, TAG, FUSE, CTX, TR>::smem_bytes(qcap, scap, ring);
+        default: return Pipe<4, AGG, TAG, FUSE, CTX, TR>::smem_bytes(qcap, scap, ring);
     }
 }
 

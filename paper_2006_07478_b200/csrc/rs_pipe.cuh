@@ -370,6 +370,7 @@ static __device__ __noinline__ void load_pv(const uint32_t *ctx, const uint32_t 
         r = ((slot & 1u) ? chunk_fr[k + 1] : chunk_fr[k]) - 1u;
     }
     const uint32_t v = ctx[r];
+    __syncwarp();          // every lane's reads of the previous value come first
     if ((threadIdx.x & 31u) == 0) *dst = v;
     __syncwarp();
 }
