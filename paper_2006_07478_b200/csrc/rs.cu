@@ -222,6 +222,7 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
                 return fail(RS_ERR_UNSUPPORTED, "PARENT_LT is built for the signal strategy (uniform context per ensemble, P:464-465)");
     if (cfg.strategy == RS_STRATEGY_AUTO) {
         rs_config c = cfg;
+        if (c.chunk == 0) c.chunk = 8192;       // both strategies share the prepass's chunk table
         rs_pipeline *a = nullptr, *b = nullptr;
         c.strategy = RS_STRATEGY_SIGNAL;
         rs_status s = rs_pipeline_create(nodes, n_nodes, elem, &c, &a);
@@ -283,7 +284,10 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
         return fail(RS_ERR_UNSUPPORTED, "queue_cap must be a power of 2 in [256, 65536]");
     if (!is_pow2(cfg.signal_cap) || cfg.signal_cap < 4 || cfg.signal_cap > 65536)
         return fail(RS_ERR_UNSUPPORTED, "signal_cap must be a power of 2 in [4, 65536]");
-    if (cfg.chunk == 0) cfg.chunk = 8192;
+    // children per claim: 2^15 for 4-byte signal / context pipelines (fewer regions split
+    // across chunks: variable L = 4096 1.84 -> 1.63 ms), 2^13 for tagged ones (R-MAT's skewed
+    // degrees balance better) and byte streams (profiles/r2_tuning.txt)
+    if (cfg.chunk == 0) cfg.chunk = (inplace && !tagged_) ? 32768 : 8192;
     if (!is_pow2(cfg.chunk) || cfg.chunk < 2048 || cfg.chunk > (1u << 24))
         return fail(RS_ERR_UNSUPPORTED, "chunk must be a power of 2 in [2048, 2^24]");
     if (cfg.grid < 0) return fail(RS_ERR_INVALID_ARG, "grid must be >= 0");

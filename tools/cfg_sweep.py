@@ -21,6 +21,7 @@ ap.add_argument("--strategy", default="signal")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--profile", action="store_true")
 ap.add_argument("--flags", type=int, default=0)
+ap.add_argument("--chunk", type=int, default=0)
 ap.add_argument("cfgs", nargs="*")
 a = ap.parse_args()
 spec = bench.workload_spec(a.workload)
@@ -32,7 +33,7 @@ for c in (a.cfgs or ["0:0:0"]):
     q, s, sc = (int(x) for x in c.split(":"))
     try:
         p = rs.Pipeline(spec["stages"], spec["agg"], strategy=a.strategy, queue_cap=q, q0_stage=s, signal_cap=sc,
-                        flags=rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING | a.flags)
+                        flags=rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING | a.flags, chunk=a.chunk)
         out = p.alloc_outputs(R, dev)
         ws = p.alloc_workspace(R, vals.numel(), dev)
         for _ in range(3):
@@ -52,7 +53,7 @@ for c in (a.cfgs or ["0:0:0"]):
                   "waits", pr[9], "instances", pr[10], " children/sweep", n / max(1, pr[8]), "refill", pr[11], "fence", pr[12],
                   "part_info", pr[13], "tma-issue", pr[14], "stages", pr[15], flush=True)
         t = statistics.median(ms)
-        print(f"{a.workload} {a.strategy} q={q} stage={s} scap={sc}: {t:.4f} ms  {n / t / 1e6:.1f} G/s  "
+        print(f"{a.workload} {a.strategy} C={a.chunk} q={q} stage={s} scap={sc}: {t:.4f} ms  {n / t / 1e6:.1f} G/s  "
               f"hbm {bench.alg_bytes(n, R, spec['agg']) / t / 1e6 / bench.hbm_peak()[0]:.3f}  err {p.check()}  {g}",
               flush=True)
         del p, out, ws
