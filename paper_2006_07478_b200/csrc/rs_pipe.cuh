@@ -584,7 +584,7 @@ struct Pipe {
         uint8_t *dst = reinterpret_cast<uint8_t *>(Q<0>()) + (size_t)(p0 & (ring0 - 1)) * ESZ;
         uint64_t *b = &bar[j & (nstg - 1)];
         uint32_t ntma = sblk;
-        if (p0 + sblk > c.pos + flen(c)) {
+        if ((int)(p0 + sblk - (c.pos + flen(c))) > 0) {   // (positions wrap: compare differences)
             // the chunk's last (short) stage; a stage inside the chunk ends at or
             // before c.end <= n_elems, so whole stages need none of this
             const uint32_t n = c.pos + flen(c) - p0;
@@ -629,10 +629,10 @@ struct Pipe {
 
     __device__ __forceinline__ void refill() {
         for (;;) {
-            if ((stg_j + 1) * sblk > oldest() + ring0) return;   // ring slots still in use
+            if ((int)((stg_j + 1) * sblk - (oldest() + ring0)) > 0) return;   // ring slots still in use
             const uint32_t sp = stg_j * sblk;
-            if (F0.k >= 0 && sp < F0.pos + flen(F0)) { issue_stage(F0); continue; }
-            if (F1.k >= 0 && sp < F1.pos + flen(F1)) { issue_stage(F1); continue; }
+            if (F0.k >= 0 && (int)(sp - (F0.pos + flen(F0))) < 0) { issue_stage(F0); continue; }   // (wrap-safe)
+            if (F1.k >= 0 && (int)(sp - (F1.pos + flen(F1))) < 0) { issue_stage(F1); continue; }
             if (F1.k >= 0 || claims_done) return;
             const int32_t k = claim();
             if (k < 0) { claims_done = true; return; }
@@ -729,7 +729,8 @@ struct Pipe {
                 prog = true;
                 continue;
             }
-            const uint32_t lim_pos = min(stg_j * sblk, F0.pos + flen(F0));
+            const uint32_t fend = F0.pos + flen(F0), sj = stg_j * sblk;
+            const uint32_t lim_pos = (int)(sj - fend) < 0 ? sj : fend;   // min, wrap-safe
             const uint32_t avail = lim_pos - E<0>().qt;
             if (!pc_valid || pidx >= pc_base + 32) {
                 pc_base = pidx;
