@@ -60,9 +60,15 @@ typedef enum {
     RS_NODE_FILTER = 2,      /* keep or drop each item (0..1 outputs per input)          */
     RS_NODE_TRANSFORM = 3,   /* rewrite each item (exactly 1 output per input)           */
     RS_NODE_AGGREGATE = 4,   /* one result per parent (begin/run/end)         */
-    RS_NODE_EMIT = 5         /* element-wise exit: every surviving item is written out with
+    RS_NODE_EMIT = 5,        /* element-wise exit: every surviving item is written out with
                                 its parent's id, "stripped of their parent context"
                                 (taxi stage 2) -- rs_pipeline_run_emit */
+    RS_NODE_SPLIT = 6        /* fan-out (tree topology, Fig. 1b): routes each item to
+                                child A (its FILTER op holds) or child B; both children follow it
+                                in the node list (pre-order) and must be AGGREGATE(SUM_I64) leaves:
+                                ENUMERATE, 0..2 stages, SPLIT, AGGREGATE, AGGREGATE.  Every signal
+                                reaches both children with per-child credits.  out.v0 = child A's
+                                int64 sums, out.v1 = child B's.  i32 elements, signal strategy. */
 } rs_node_kind;
 
 /* Operations.  The paper leaves isGood() and the aggregate open (P:529,
@@ -193,7 +199,8 @@ rs_status rs_config_default(rs_config *cfg);
 
 /* Build a pipeline from a node list (BASELINE north star: "create pipeline
  * from a node list").  The list must be ENUMERATE, then 0..4 FILTER/TRANSFORM
- * nodes, then one AGGREGATE (single-level enumeration).  `elem` is the
+ * nodes, then one AGGREGATE or EMIT (single-level enumeration) -- or, for a
+ * tree, ENUMERATE, 0..2 stages, SPLIT and its two AGGREGATE leaves.  `elem` is the
  * element type of the parents' payload.  Errors: RS_ERR_INVALID_TOPOLOGY,
  * RS_ERR_UNSUPPORTED (op/dtype mismatch, w != 128, capacities), RS_ERR_INVALID_ARG. */
 rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem,

@@ -89,6 +89,7 @@ def lib():
         L.or_emit.argtypes = [i32, vp, vp, i64, vp, i32, vp, vp, i64]
         L.or_emit.restype = i64
         L.or_emit_pair.argtypes = [vp, vp, i64, vp, i32, vp, vp, i64]
+        L.or_brute_split.argtypes = [i32, vp, vp, i64, vp, i32, vp, vp, vp]
         L.or_emit_pair.restype = i64
         L.or_interp.argtypes = [i32, vp, vp, i64, vp, i32, i32, i32, i64, i64, i64, i32, u64, i32,
                                 vp, vp, vp, vp, i64, vp]
@@ -184,6 +185,23 @@ def brute(elems, offsets, stages, agg):
     if rc:
         raise OracleError(ERRORS.get(rc, rc))
     return o0, o1
+
+
+def brute_split(elems, offsets, stages, split):
+    """Fan-out (Fig. 1b): per region, the int64 sums of the
+    survivors of `stages` that pass (child A) / fail (child B) the `split`
+    FILTER op."""
+    elems, offsets = _prep(elems, offsets)
+    R = offsets.size - 1
+    st, keep = _stages(stages)
+    sp, keep2 = _stages([split])
+    a = np.zeros(R, np.int64)
+    b = np.zeros(R, np.int64)
+    rc = lib().or_brute_split(DTYPES[_dtype_name(elems)], _ptr(elems), _ptr(offsets), R, C.addressof(st),
+                              len(stages), C.addressof(sp), _ptr(a), _ptr(b))
+    if rc:
+        raise OracleError(ERRORS.get(rc, rc))
+    return a, b
 
 
 def emit(elems, offsets, stages):

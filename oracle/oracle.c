@@ -202,6 +202,30 @@ int or_node_counts(int dtype, const void *elems, const int64_t *off, int64_t R,
     return OR_OK;
 }
 
+/* Fan-out (tree topology, Fig. 1b): after the
+ * stages, a SPLIT node sends each item to child A if its op holds, else to
+ * child B; both children are SUM_I64 aggregates, so the plain definition is
+ * two per-region folds over the two partitions of each region's survivors.  */
+int or_brute_split(int dtype, const void *elems, const int64_t *off, int64_t R, const or_stage *st, int nst,
+                   const or_stage *split, int64_t *out_a, int64_t *out_b) {
+    int rc = check_args(dtype, elems, off, R, st, nst, OR_SUM_I64);
+    if (rc || !split) return rc ? rc : OR_EARG;
+    for (int64_t r = 0; r < R; r++) {
+        int64_t a = 0, b = 0;
+        for (int64_t g = off[r]; g < off[r + 1]; g++) {
+            uint32_t v = get_item(dtype, elems, g);
+            int keep = 1;
+            for (int k = 0; k < nst && keep; k++) keep = apply_stage(&st[k], &v, r);
+            if (!keep) continue;
+            if (apply_stage(split, &v, r)) a = (int64_t)((uint64_t)a + (uint64_t)(int64_t)(int32_t)v);
+            else b = (int64_t)((uint64_t)b + (uint64_t)(int64_t)(int32_t)v);
+        }
+        out_a[r] = a;
+        out_b[r] = b;
+    }
+    return OR_OK;
+}
+
 /* Element-wise exit: instead of one result per parent, a
  * stream of results derived from individual elements, "stripped of their
  * parent context" (§4; the taxi app's second stage emits each

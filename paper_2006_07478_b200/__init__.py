@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("RS_LIB") or os.path.join(_HERE, "lib", "librs.so")
 # rs.h enumerations (kept in sync with include/rs.h by tests/test_abi.py)
 RS_OK, RS_ERR_INVALID_ARG, RS_ERR_INVALID_TOPOLOGY, RS_ERR_UNSUPPORTED = 0, -1, -2, -3
 RS_ERR_WORKSPACE, RS_ERR_CUDA, RS_ERR_PROTOCOL, RS_ERR_NCCL = -4, -5, -6, -7
-RS_NODE_ENUMERATE, RS_NODE_FILTER, RS_NODE_TRANSFORM, RS_NODE_AGGREGATE, RS_NODE_EMIT = 1, 2, 3, 4, 5
+RS_NODE_ENUMERATE, RS_NODE_FILTER, RS_NODE_TRANSFORM, RS_NODE_AGGREGATE, RS_NODE_EMIT, RS_NODE_SPLIT = 1, 2, 3, 4, 5, 6
 OPS = {"none": 0, "hash_lt": 1, "lt_u32": 2, "class": 3, "parent_lt": 4, "scale_f32": 10, "affine_i32": 11,
        "sum_i64": 20, "sum_f32": 21, "count_min_u32": 22, "count_xor64": 23, "emit_value": 24, "emit_pair": 25}
 DTYPES = {"i32": 0, "u32": 1, "u8": 2, "f32": 3}
@@ -147,7 +147,7 @@ def _node(spec) -> tuple:
     raise ValueError(f"unknown stage {name}")
 
 
-AGG_ELEM = {"sum_i64": "i32", "sum_f32": "f32", "count_min_u32": "u32", "count_xor64": "u8", "emit_value": "i32",
+AGG_ELEM = {"split_sum_i64": "i32", "sum_i64": "i32", "sum_f32": "f32", "count_min_u32": "u32", "count_xor64": "u8", "emit_value": "i32",
             "emit_pair": "u8"}
 
 
@@ -156,12 +156,15 @@ class Pipeline:
     ``agg``: aggregate op name.  Node list = [ENUMERATE] + stages + [AGGREGATE]."""
 
     def __init__(self, stages, agg, elem=None, strategy="signal", queue_cap=0, signal_cap=0, grid=0,
-                 chunk=0, flags=RS_FLAG_STATS, simd_width=128, q0_stage=0, auto_min_len=0, tag_from=0):
+                 chunk=0, flags=RS_FLAG_STATS, simd_width=128, q0_stage=0, auto_min_len=0, tag_from=0, split=None):
+        """agg "split_sum_i64" builds a tree (RS_NODE_SPLIT): `split` is the
+        FILTER-op tuple that routes an item to child A (v0) or child B (v1)."""
         L = lib()
         self.stages = list(stages)
         self.agg = agg
         self.elem = elem or AGG_ELEM[agg]
-        nodes = (rs_node * (len(self.stages) + 2))()
+        tree = agg == "split_sum_i64"
+        nodes = (rs_node * (len(self.stages) + (4 if tree else 2)))()
         self._tables = []
         nodes[0] = rs_node(RS_NODE_ENUMERATE, 0, 0, 0, None)
         for i, s in enumerate(self.stages):
@@ -172,7 +175,13 @@ class Pipeline:
                 self._tables.append(buf)
                 tp = C.addressof(buf)
             nodes[i + 1] = rs_node(kind, op, p0, p1, tp)
-        nodes[-1] = rs_node(RS_NODE_EMIT if agg.startswith("emit") else RS_NODE_AGGREGATE, OPS[agg], 0, 0, None)
+        if tree:
+            kind, op, p0, p1, _ = _node(split)
+            nodes[len(self.stages) + 1] = rs_node(RS_NODE_SPLIT, op, p0, p1, None)
+            nodes[-2] = rs_node(RS_NODE_AGGREGATE, OPS["sum_i64"], 0, 0, None)
+            nodes[-1] = rs_node(RS_NODE_AGGREGATE, OPS["sum_i64"], 0, 0, None)
+        else:
+            nodes[-1] = rs_node(RS_NODE_EMIT if agg.startswith("emit") else RS_NODE_AGGREGATE, OPS[agg], 0, 0, None)
         cfg = rs_config()
         L.rs_config_default(C.byref(cfg))
         cfg.strategy = STRATEGIES[strategy]
@@ -188,9 +197,9 @@ class Pipeline:
         cfg.auto_min_len = auto_min_len
         cfg.tag_from = tag_from
         h = C.c_void_p()
-        _check(L.rs_pipeline_create(nodes, len(self.stages) + 2, DTYPES[self.elem], C.byref(cfg), C.byref(h)))
+        _check(L.rs_pipeline_create(nodes, len(nodes), DTYPES[self.elem], C.byref(cfg), C.byref(h)))
         self.h = h
-        self.n_nodes = len(self.stages) + 2
+        self.n_nodes = len(nodes)
         self.strategy = strategy
 
     def close(self):
@@ -220,6 +229,9 @@ class Pipeline:
         import torch
         if self.agg == "sum_i64":
             return torch.empty(n_regions, dtype=torch.int64, device=device), None
+        if self.agg == "split_sum_i64":
+            return (torch.empty(n_regions, dtype=torch.int64, device=device),
+                    torch.empty(n_regions, dtype=torch.int64, device=device))
         if self.agg == "sum_f32":
             return torch.empty(n_regions, dtype=torch.float32, device=device), None
         if self.agg == "count_min_u32":

@@ -59,6 +59,8 @@ struct rs_pipeline {
 
 namespace {
 
+constexpr int AGG_SPLIT = 26;   // internal aggregate id of a fan-out (tree) pipeline
+
 // Process-wide: the dynamic shared-memory limit of a kernel is a per-function
 // attribute, so it is raised once per (kernel, device) to the opt-in maximum
 // under a lock; launches and occupancy probes then only ever ask for less
@@ -88,6 +90,10 @@ uint32_t auto_default(int nst) {
 }
 
 bool get_launch(const rs_pipeline *p, Launch *L) {
+    if (p->agg == AGG_SPLIT) {
+        *L = launch_agg26_split(p->nst, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage);
+        return L->main != nullptr;
+    }
     if (p->cfg.strategy == RS_STRATEGY_HYBRID) {
         const bool fuse = (p->cfg.flags & RS_FLAG_UNFUSED) == 0;
         if (p->agg == RS_OP_SUM_I64)
@@ -178,6 +184,46 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     rs_config cfg;
     if (cfg_in) cfg = *cfg_in; else rs_config_default(&cfg);
     if (nodes[0].kind != RS_NODE_ENUMERATE) return fail(RS_ERR_INVALID_TOPOLOGY, "node 0 must be ENUMERATE");
+    // tree (fan-out): ENUMERATE, stages, SPLIT, AGGREGATE (child A), AGGREGATE (child B)
+    int split_at = -1;
+    for (int i = 1; i < n_nodes; ++i)
+        if (nodes[i].kind == RS_NODE_SPLIT) {
+            if (split_at >= 0) return fail(RS_ERR_INVALID_TOPOLOGY, "one SPLIT node per pipeline is built");
+            split_at = i;
+        }
+    if (split_at >= 0) {
+        if (split_at != n_nodes - 3 || nodes[n_nodes - 2].kind != RS_NODE_AGGREGATE ||
+            nodes[n_nodes - 1].kind != RS_NODE_AGGREGATE)
+            return fail(RS_ERR_INVALID_TOPOLOGY, "a SPLIT node's two children must be AGGREGATE leaves following it");
+        if (nodes[n_nodes - 2].op != RS_OP_SUM_I64 || nodes[n_nodes - 1].op != RS_OP_SUM_I64 || elem != RS_I32)
+            return fail(RS_ERR_UNSUPPORTED, "the fan-out is built for i32 elements and SUM_I64 leaves");
+        if (split_at - 1 > 2) return fail(RS_ERR_UNSUPPORTED, "at most 2 stages before a SPLIT are built");
+        if (cfg.strategy != RS_STRATEGY_SIGNAL || (cfg.flags & (RS_FLAG_TRACE | RS_FLAG_PROFILE)))
+            return fail(RS_ERR_UNSUPPORTED, "the fan-out is built for the signal strategy");
+        const int sop = nodes[split_at].op;
+        if (sop != RS_OP_HASH_LT && sop != RS_OP_LT_U32 && sop != RS_OP_PARENT_LT)
+            return fail(RS_ERR_UNSUPPORTED, "SPLIT ops: HASH_LT, LT_U32, PARENT_LT");
+        for (int i = 1; i < split_at; ++i)
+            if (nodes[i].kind != RS_NODE_FILTER && nodes[i].kind != RS_NODE_TRANSFORM)
+                return fail(RS_ERR_INVALID_TOPOLOGY, "only FILTER/TRANSFORM nodes may precede a SPLIT");
+        // validate and store the stages and the split op like a linear pipeline with the
+        // split as its last stage (st[K] = the split op)
+        rs_node lin[MAXK + 2];
+        for (int i = 0; i <= split_at; ++i) lin[i] = nodes[i];
+        lin[split_at].kind = RS_NODE_FILTER;
+        lin[split_at + 1] = nodes[n_nodes - 1];              // an AGGREGATE(SUM_I64) closes the check list
+        rs_config c = cfg;
+        c.flags |= RS_FLAG_UNFUSED;
+        if (c.queue_cap == 0) c.queue_cap = 8 * W;            // in-place ring and each child's queue
+        rs_pipeline *q = nullptr;
+        rs_status st = rs_pipeline_create(lin, split_at + 2, elem, &c, &q);
+        if (st != RS_OK) return st;
+        q->n_nodes = n_nodes;
+        q->nst = split_at - 1;                                // stages before the split; st[nst] = split op
+        q->agg = AGG_SPLIT;
+        *out = q;
+        return RS_OK;
+    }
     if (nodes[n_nodes - 1].kind != RS_NODE_AGGREGATE && nodes[n_nodes - 1].kind != RS_NODE_EMIT)
         return fail(RS_ERR_INVALID_TOPOLOGY, "last node must be AGGREGATE or EMIT");
     const bool emit_ = nodes[n_nodes - 1].kind == RS_NODE_EMIT;

@@ -239,7 +239,38 @@ struct AggT<24> {  // RS_OP_EMIT_VALUE: element-wise exit -- no per-region fold 
 };
 
 template <>
-struct AggT<25> : AggT<24> {};   // RS_OP_EMIT_PAIR: element-wise exit of parsed "{x,y}" pairs (u8)
+struct AggT<25> : AggT<24> {};
+
+// Fan-out (SPLIT node with two leaf SUM_I64 aggregates): the pair of sums, for
+// the split-region partial slots and the fixup (v0 = child A, v1 = child B).
+template <>
+struct AggT<26> {
+    static constexpr bool heavy = false;
+    static constexpr bool group = true;
+    using A = ulonglong2;
+    __device__ static A id() { return make_ulonglong2(0ull, 0ull); }
+    __device__ static A lift(uint32_t) { return id(); }
+    __device__ static A lift_i(uint32_t, long long) { return id(); }
+    __device__ static A comb(A a, A b) { return make_ulonglong2(a.x + b.x, a.y + b.y); }
+    __device__ static A sub(A a, A b) { return make_ulonglong2(a.x - b.x, a.y - b.y); }
+    __device__ static A shfl(A a, int src) {
+        return make_ulonglong2(__shfl_sync(kFull, a.x, src), __shfl_sync(kFull, a.y, src));
+    }
+    __device__ static A shfl_up(A a, int d) {
+        return make_ulonglong2(__shfl_up_sync(kFull, a.x, d), __shfl_up_sync(kFull, a.y, d));
+    }
+    __device__ static A shfl_xor(A a, int m) {
+        return make_ulonglong2(__shfl_xor_sync(kFull, a.x, m), __shfl_xor_sync(kFull, a.y, m));
+    }
+    __device__ static void store(void *o0, void *o1, uint64_t i, A a) {
+        ((unsigned long long *)o0)[i] = a.x;
+        ((unsigned long long *)o1)[i] = a.y;
+    }
+    __device__ static A load(const void *o0, const void *o1, uint64_t i) {
+        return make_ulonglong2(((const unsigned long long *)o0)[i], ((const unsigned long long *)o1)[i]);
+    }
+    static constexpr int bytes0 = 8, bytes1 = 8;
+};   // RS_OP_EMIT_PAIR: element-wise exit of parsed "{x,y}" pairs (u8)
 
 template <class AT>
 __device__ __forceinline__ typename AT::A warp_reduce(typename AT::A a) {

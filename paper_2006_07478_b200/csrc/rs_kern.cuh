@@ -231,6 +231,8 @@ Launch launch_agg20_trace(int K, bool fuse, uint32_t qcap, uint32_t scap, uint32
 // RS_STRATEGY_HYBRID instantiations (edges >= hyb carry tags; rs_k20h.cu, rs_k25h.cu)
 Launch launch_agg20_hybrid(int K, bool fuse, int hyb, uint32_t qcap, uint32_t scap, uint32_t sblk);
 Launch launch_agg25_hybrid(int K, bool fuse, int hyb, uint32_t qcap, uint32_t scap, uint32_t sblk);
+// fan-out (SPLIT + two leaf SUM_I64 aggregates; rs_k26.cu), K <= 2 stages before the split
+Launch launch_agg26_split(int K, uint32_t qcap, uint32_t scap, uint32_t sblk);
 
 #ifndef RS_HOST_ONLY
 // Hybrid kernels: K stages, edges >= hyb tagged (1 <= hyb <= the aggregating

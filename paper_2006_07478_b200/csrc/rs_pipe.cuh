@@ -375,13 +375,18 @@ static __device__ __noinline__ void load_pv(const uint32_t *ctx, const uint32_t 
     __syncwarp();
 }
 
-template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false, int HYB = 0>
+template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false, int HYB = 0, bool SPL = false>
 struct Pipe {
     using AT = AggT<AGG>;
     using A = typename AT::A;
     static constexpr bool NA = FUSE && K >= 1;        // aggregate fused into node K
     static constexpr int NQ = NA ? K - 1 : K;         // shared-memory data queues Q_1..Q_NQ
     static constexpr int NSG = NA ? K : K + 1;        // signal rings S_0..S_{NSG-1}
+    // Fan-out (§8 f4, Fig. 1b): SPL pipelines end in a SPLIT node
+    // (node K+1) with two leaf AGGREGATE children (nodes K+2, K+3) fed by edges
+    // K+1 and K+2, each a queue and a signal queue of its own (separate rings
+    // after the in-place ring).
+    static constexpr int NLQ = SPL ? 2 : 0;
     // Per-stage hybrid (§8 f1; the paper's best taxi variant signals through
     // stage 1 and tags from stage 2 on): HYB >= 1 makes
     // edges 0..HYB-1 signal-delimited and edges HYB.. tagged; node HYB
@@ -456,7 +461,8 @@ struct Pipe {
     // strategy, then the signal rings.  In-place: every Q_e is the Q0 ring.
     static constexpr uint32_t NQS = INPLACE ? 0 : NQ;   // separate shared-memory queues
     template <int e> __device__ __forceinline__ uint32_t *Q() const {
-        if constexpr (e == 0 || INPLACE) return reinterpret_cast<uint32_t *>(base + HDR);
+        if constexpr (SPL && e > K) return reinterpret_cast<uint32_t *>(base + HDR + q0_bytes(ring0) + (e - K - 1) * qcap * 4);
+        else if constexpr (e == 0 || INPLACE) return reinterpret_cast<uint32_t *>(base + HDR);
         else return reinterpret_cast<uint32_t *>(base + HDR + q0_bytes(ring0) + (TAGANY ? ring0 * 4 : 0) +
                                                  (e - 1) * qcap * 4 * (TAGANY ? 2 : 1));
     }
@@ -466,11 +472,14 @@ struct Pipe {
         else return Q<e>() + qcap;
     }
     template <int e> __device__ __forceinline__ uint2 *S() const {
-        return reinterpret_cast<uint2 *>(base + HDR + q0_bytes(ring0) + (TAGANY ? ring0 * 4 : 0) + NQS * qcap * 4 * (TAGANY ? 2 : 1)) +
+        return reinterpret_cast<uint2 *>(base + HDR + q0_bytes(ring0) + (TAGANY ? ring0 * 4 : 0) + NQS * qcap * 4 * (TAGANY ? 2 : 1) +
+                                         NLQ * qcap * 4) +
                e * scap;
     }
     // ring index mask of edge e's queue
-    template <int e> __device__ __forceinline__ uint32_t qm() const { return (e == 0 || INPLACE) ? ring0 - 1 : qmask; }
+    template <int e> __device__ __forceinline__ uint32_t qm() const {
+        return (SPL && e > K) ? qmask : ((e == 0 || INPLACE) ? ring0 - 1 : qmask);
+    }
 
     Chunk F0, F1;                      // chunk being enumerated, chunk staged next
     bool claims_done, enum_done;
@@ -493,7 +502,7 @@ struct Pipe {
     uint32_t ckey = 0; // hybrid converter node: key of the open region
     long long base0, offR, off0;
     uint32_t nchunks;
-    uint32_t q_start[K + 1];       // initial queue positions (edge 0 may start at the chunk-0 pad)
+    uint32_t q_start[K + 1 + NLQ]; // initial queue positions (edge 0 may start at the chunk-0 pad)
     // RS_FLAG_PROFILE: cycles spent per node (0 = enumerate, 1..K+1, K+2 = TMA wait)
     // RS_FLAG_PROFILE cycle counters exist in the debug (TR) instantiations
     // only: the production kernels carry no profiling code (i-cache).
@@ -514,7 +523,7 @@ struct Pipe {
         bar = reinterpret_cast<uint64_t *>(smem);
         E0 = E1 = E2 = E3 = E4 = EdgeS{0u, 0u, 0u, 0u, 0u, 0u, false};
 #pragma unroll
-        for (int e = 0; e <= K; ++e) q_start[e] = 0u;
+        for (int e = 0; e <= K + NLQ; ++e) q_start[e] = 0u;
         for (int i = 16 + lane; i < (int)(HDR / 4); i += 32) reinterpret_cast<uint32_t *>(base)[i] = 0u;   // counters + profile
         __syncwarp();
         F0.k = F1.k = -1;
@@ -538,7 +547,7 @@ struct Pipe {
 
     __host__ __device__ static constexpr uint32_t smem_bytes(uint32_t qcap, uint32_t scap, uint32_t ring) {
         return HDR + q0_bytes(ring) + (TAGANY ? ring * 4 : 0) + NQS * qcap * 4 * (TAGANY ? 2 : 1) +
-               (TAG ? 0 : NSG * scap * 8);
+               (TAG ? 0 : NSG * scap * 8) + NLQ * (qcap * 4 + scap * 8);
     }
     // Ring capacity: 4 TMA stages; in-place, the configured queue capacity
     // (the one ring all queues share), at most NSTMAX stages, and at least one
@@ -1371,6 +1380,168 @@ struct Pipe {
         }
     }
 
+    // --------------------------------------------------- fan-out (SPL)
+    // A tree topology (Fig. 1b; §8 f4): the SPLIT node (node K+1)
+    // sends every item of its ensembles to child A (its op holds) or child B
+    // (it does not) -- two stable ballot/popc compactions into the children's
+    // queues -- and forwards every signal to BOTH children, each with the
+    // credit of its own edge (items sent to that child since its last signal,
+    // P:304-312), so each child sees its own precisely delimited regions
+    // (P:151-159).  The children are leaf AGGREGATEs (SUM_I64): A's sums go to
+    // out.v0, B's to out.v1.
+    unsigned long long lacc0 = 0, lacc1 = 0;    // leaf A / B per-lane partial sums
+    template <class Op>
+    __device__ __forceinline__ void split_ens(const Op &op, const uint32_t *in, uint32_t imask, uint32_t h, uint32_t e) {
+        constexpr int ea = K + 1, eb = K + 2;
+        uint32_t *qa = Q<ea>(), *qb = Q<eb>();
+        uint32_t ta = E<ea>().qt, tb = E<eb>().qt;
+#pragma unroll
+        for (int j = 0; j < IPL; ++j) {
+            if ((uint32_t)j * 32u >= e) break;
+            const bool act = (uint32_t)(j * 32 + lane) < e;
+            uint32_t v = act ? in[(h + j * 32 + lane) & imask] : 0u;
+            const bool keep = act && op(v);
+            const uint32_t ka = __ballot_sync(kFull, keep), kb = __ballot_sync(kFull, act && !keep);
+            if (keep) qa[(ta + __popc(ka & lt)) & qmask] = v;
+            else if (act) qb[(tb + __popc(kb & lt)) & qmask] = v;
+            ta += __popc(ka);
+            tb += __popc(kb);
+        }
+        __syncwarp();
+        E<ea>().sent += ta - E<ea>().qt;
+        E<ea>().qt = ta;
+        E<eb>().sent += tb - E<eb>().qt;
+        E<eb>().qt = tb;
+    }
+    __device__ __forceinline__ bool fire_split(bool drained) {
+        constexpr int ei = K, ea = K + 1, eb = K + 2, n = K + 1;
+        const uint32_t imask = qm<ei>();
+        const uint32_t *in = Q<ei>();
+        bool prog = false;
+        uint32_t ready_lim = 0;
+        if (ei == 0) ready_lim = landed_pos();
+        for (;;) {
+            bool spend;
+            const uint32_t a = admissible<ei>(spend);
+            uint32_t ar = a;
+            if (ei == 0) {
+                if ((int)(ready_lim - E<0>().qh) < (int)ar) ready_lim = landed_pos();
+                const int rdy = (int)(ready_lim - E<0>().qh);
+                ar = rdy <= 0 ? 0u : min(ar, (uint32_t)rdy);
+            }
+            const uint32_t space = min(qcap - (E<ea>().qt - E<ea>().qh), qcap - (E<eb>().qt - E<eb>().qh));
+            uint32_t lim = min(ar, space), arem = a;
+            bool did = false;
+            while (lim >= (uint32_t)W) {
+                with_op_k(P.st[K], pvn(n), [&](auto op) { split_ens(op, in, imask, E<ei>().qh, W); });
+                E<ei>().qh += W;
+                if (spend) E<ei>().cur -= W;
+                lim -= W;
+                arem -= W;
+                did = true;
+            }
+            if (lim > 0 && ((spend && lim == E<ei>().cur) || (drained && lim == arem))) {
+                with_op_k(P.st[K], pvn(n), [&](auto op) { split_ens(op, in, imask, E<ei>().qh, lim); });
+                E<ei>().qh += lim;
+                if (spend) E<ei>().cur -= lim;
+                stat_add(n, 0, 1u);
+                stat_add(n, 1, lim);
+                did = true;
+            }
+            if (!spend || E<ei>().cur != 0) {
+                if (!did) break;
+                prog = true;
+                continue;
+            }
+            uint32_t nsig = 0;
+            for (;;) {
+                if (scap - (E<ea>().st - E<ea>().sh) == 0 || scap - (E<eb>().st - E<eb>().sh) == 0) break;
+                const uint2 hs = S<ei>()[E<ei>().sh & smask];
+                E<ei>().sh++;
+                E<ei>().xfer = false;
+                ++nsig;
+                const bool is_end = (hs.y & END_BIT) != 0;
+                if (!is_end && P.st[K].op == RS_OP_PARENT_LT) set_pv(n, hs.x);
+                push_signal<ea>(hs.x, is_end, E<ea>().sent);     // each child: its own credit
+                push_signal<eb>(hs.x, is_end, E<eb>().sent);
+                if (E<ei>().sh == E<ei>().st) break;
+                const uint32_t c = S<ei>()[E<ei>().sh & smask].y & ~END_BIT;
+                if (c > 0) {
+                    E<ei>().cur = c;
+                    E<ei>().xfer = true;
+                    break;
+                }
+            }
+            if (nsig == 0 && !did) break;
+            prog = true;
+        }
+        __syncwarp();
+        return prog;
+    }
+    // leaf AGGREGATE on edge e (SUM_I64 of its items, per region)
+    template <int e>
+    __device__ __forceinline__ bool fire_leaf(bool drained) {
+        constexpr int n = e + 1;
+        constexpr bool B = (e == K + 2);
+        unsigned long long &la = B ? lacc1 : lacc0;
+        const uint32_t *in = Q<e>();
+        bool prog = false;
+        for (;;) {
+            bool spend;
+            const uint32_t a = admissible<e>(spend);
+            uint32_t lim = a, arem = a, take = 0;
+            bool did = false;
+            if (lim >= (uint32_t)W) take = lim & ~(uint32_t)(W - 1);
+            if (lim > take && ((spend && lim == E<e>().cur) || (drained && lim == arem))) {
+                stat_add(n, 0, 1u);
+                stat_add(n, 1, lim - take);
+                take = lim;
+            }
+            if (take) {
+                const uint32_t h = E<e>().qh;
+                for (uint32_t i = lane; i < take; i += 32) la += (unsigned long long)(long long)(int)in[(h + i) & qmask];
+                E<e>().qh += take;
+                if (spend) E<e>().cur -= take;
+                did = true;
+            }
+            if (!spend || E<e>().cur != 0) {
+                if (!did) break;
+                prog = true;
+                continue;
+            }
+            uint32_t nsig = 0;
+            for (;;) {
+                const uint2 hs = S<e>()[E<e>().sh & smask];
+                E<e>().sh++;
+                E<e>().xfer = false;
+                ++nsig;
+                if (hs.y & END_BIT) {                 // a::end: this child's result for the region
+                    unsigned long long v = la;
+#pragma unroll
+                    for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(kFull, v, m);
+                    if (lane == 0) {
+                        const uint32_t key = hs.x;
+                        unsigned long long *o = reinterpret_cast<unsigned long long *>(
+                            (key & SLOT) ? (B ? P.part1 : P.part0) : (B ? P.out1 : P.out0));
+                        o[key & ~SLOT] = v;
+                    }
+                }
+                la = 0;                               // a::begin / after a::end
+                if (E<e>().sh == E<e>().st) break;
+                const uint32_t c = S<e>()[E<e>().sh & smask].y & ~END_BIT;
+                if (c > 0) {
+                    E<e>().cur = c;
+                    E<e>().xfer = true;
+                    break;
+                }
+            }
+            if (nsig == 0 && !did) break;
+            prog = true;
+        }
+        __syncwarp();
+        return prog;
+    }
+
     // ----------------------------------------------- per-lane context (CTX)
     // Close the open region (akey: uniform partial `carry` + per-lane `acc`)
     // and open `key` (a::end then a::begin).
@@ -1776,7 +1947,7 @@ struct Pipe {
 
     template <int k = 0>
     __device__ __forceinline__ bool all_empty() const {
-        if constexpr (k > K) {
+        if constexpr (k > K + NLQ) {
             return true;
         } else {
             return (E<k>().qh == E<k>().qt) && (E<k>().sh == E<k>().st) && all_empty<k + 1>();
@@ -1805,7 +1976,13 @@ struct Pipe {
 
     template <int n>
     __device__ __forceinline__ bool fire_chain(bool drained) {
-        if constexpr (n > (NA ? K : K + 1)) {
+        if constexpr (SPL && n == K + 1) {
+            bool p = fire_split(drained);
+            const bool dn = drained && (E<K>().qh == E<K>().qt) && (E<K>().sh == E<K>().st);
+            p |= fire_leaf<K + 1>(dn);
+            p |= fire_leaf<K + 2>(dn);
+            return p;
+        } else if constexpr (n > (NA ? K : K + 1)) {
             return false;
         } else {
             const long long t0 = prof ? clock64() : 0;
@@ -1822,7 +1999,7 @@ struct Pipe {
     // full ensembles + partial ensembles (counted separately in the header).
     template <int n = 1>
     __device__ __forceinline__ void finish_counters(uint32_t fitems) {
-        if constexpr (n <= K + 1) {
+        if constexpr (n <= K + 1 + NLQ) {
             if (lane == 0) {
                 // c[0] = partial ensembles, c[1] = their items (accumulated in the run)
                 uint32_t *c = reinterpret_cast<uint32_t *>(base + CNT_OFF) + 4 * n;
@@ -1850,7 +2027,7 @@ struct Pipe {
         const uint32_t fitems = NA ? __reduce_add_sync(kFull, fkept) : 0u;
         finish_counters<1>(fitems);
         __syncwarp();
-        if (lane < K + 2) {
+        if (lane < K + 2 + NLQ) {
             const uint32_t *c = reinterpret_cast<const uint32_t *>(base + CNT_OFF) + 4 * lane;
             unsigned long long *S = P.stats + 4 * lane;
 #pragma unroll
@@ -1911,12 +2088,12 @@ struct Pipe {
     }
 };
 
-template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false, int HYB = 0>
+template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false, int HYB = 0, bool SPL = false>
 __global__ void __launch_bounds__(WPB_MAX * 32, 1) k_pipeline(const __grid_constant__ KParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    using PP = Pipe<K, AGG, TAG, FUSE, CTX, TR, HYB>;
+    using PP = Pipe<K, AGG, TAG, FUSE, CTX, TR, HYB, SPL>;
     uint8_t *mine = smem + (size_t)warp * PP::smem_bytes(P.qcap, P.scap, P.ring0);
     if (P.hdr->err) return;
     if (P.auto_sel && P.hdr->sel != P.auto_sel - 1) return;   // AUTO: the other strategy's kernel runs

@@ -614,3 +614,45 @@ def test_taxi_hybrid(rs, mode):
     st = p.stats()
     assert st[2][1] >= 0.9 * st[2][0]          # stage 2 on tagged items: full ensembles
     assert st[1][1] >= 0.8 * st[1][0]          # stage 1 (long lines, signal-delimited): mostly full (91%)
+
+
+@pytest.mark.parametrize("nst", [0, 1, 2])
+@pytest.mark.parametrize("L,dist", [(3, "var"), (200, "zipf"), (5000, "var")])
+def test_tree_fanout(rs, nst, L, dist):
+    """Tree topology (Fig. 1b): a SPLIT node routes each
+    item to leaf A or leaf B; every Begin/End reaches both leaves with per-child
+    credits.  Both leaves' per-region sums equal the oracle's, bit-exactly, over
+    short, skewed and chunk-spanning regions with empty ones; every region is
+    bracketed at both leaves (each leaf consumes 2 signals per region part)."""
+    lens = synth.lengths(max(8, (1 << 17) // L), dist, L=L, seed=L + nst, zipf_max=max(2, 2 * L))
+    lens[::7] = 0
+    off = synth.offsets(lens, base=1)
+    vals = synth.values(int(off[-1]) + 2, "i32", seed=nst + 3)
+    stages = synth.sweep_stages(nst)
+    split = ("hash_lt", 0x27D4EB2F, 128)
+    ra, rb = oracle.brute_split(vals, off, stages, split)
+    for cfg in (dict(chunk=2048), dict(chunk=4096, queue_cap=256, signal_cap=4, q0_stage=128, grid=2)):
+        p = rs.Pipeline(stages, "split_sum_i64", split=split, **cfg)
+        e = torch.from_numpy(vals).cuda()
+        o = torch.from_numpy(off).cuda()
+        R = off.size - 1
+        out = p.alloc_outputs(R)
+        ws = p.alloc_workspace(R, e.numel())
+        p.run(e, o, out, ws)
+        torch.cuda.synchronize()
+        assert p.check() == 0
+        np.testing.assert_array_equal(out[0].cpu().numpy(), ra)
+        np.testing.assert_array_equal(out[1].cpu().numpy(), rb)
+        st = p.stats()
+        assert st.shape[0] == nst + 4
+        kc = oracle.node_counts(vals, off, stages)
+        assert st[nst + 1][2] == kc[:, nst].sum()                 # the split consumes the survivors
+        assert st[nst + 2][2] + st[nst + 3][2] == kc[:, nst].sum()  # and partitions them
+        assert st[nst + 2][3] == st[nst + 3][3] == st[nst + 1][3]   # both children see every signal
+
+
+def test_tree_rejected_shapes(rs):
+    with pytest.raises(rs.RSError):
+        rs.Pipeline(synth.sweep_stages(3), "split_sum_i64", split=("hash_lt", 3, 100))   # > 2 stages before SPLIT
+    with pytest.raises(rs.RSError):
+        rs.Pipeline([], "split_sum_i64", split=("hash_lt", 3, 100), strategy="tagged")

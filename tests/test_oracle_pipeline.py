@@ -470,3 +470,25 @@ def test_emit_pair_by_construction():
     # without stage 1 every byte is tried: the same pairs (only '{' can start one)
     yx2, r2 = oracle.emit_pair(b, off, [])
     np.testing.assert_array_equal(np.stack([r2, yx2[:, 0], yx2[:, 1]], 1), exp)
+
+
+# ------------------------------------------------------ fan-out (tree, f4)
+def test_brute_split_partitions_the_survivors():
+    """Tree topology (Fig. 1b): the two leaves' sums partition each
+    region's survivors -- pinned to the numpy prefix identity of the masked
+    values (child A: split op holds, child B: it does not) and to A + B = the
+    linear pipeline's sum."""
+    lens = synth.lengths(800, "zipf", seed=6, zipf_max=400)
+    lens[::6] = 0
+    off = synth.offsets(lens, base=3)
+    vals = synth.values(int(off[-1]), "i32", seed=7)
+    stages = [("hash_lt", 0x9E3779B1, 192)]
+    a, b = oracle.brute_split(vals, off, stages, ("lt_u32", 1 << 31))
+    u = vals.view(np.uint32).astype(np.uint64)
+    keep = ((u * 0x9E3779B1) % (1 << 32)) >> 24 < 192
+    A = np.where(keep & (u < (1 << 31)), vals.astype(np.int64), 0)
+    B = np.where(keep & (u >= (1 << 31)), vals.astype(np.int64), 0)
+    for arr, got in ((A, a), (B, b)):
+        P = np.concatenate([[0], np.cumsum(arr)])
+        np.testing.assert_array_equal(got, P[off[1:]] - P[off[:-1]])
+    np.testing.assert_array_equal(a + b, oracle.brute(vals, off, stages, "sum_i64")[0])
