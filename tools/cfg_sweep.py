@@ -22,6 +22,7 @@ ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--profile", action="store_true")
 ap.add_argument("--flags", type=int, default=0)
 ap.add_argument("--chunk", type=int, default=0)
+ap.add_argument("--tag-from", type=int, default=0)
 ap.add_argument("cfgs", nargs="*")
 a = ap.parse_args()
 spec = bench.workload_spec(a.workload)
@@ -33,7 +34,7 @@ for c in (a.cfgs or ["0:0:0"]):
     q, s, sc = (int(x) for x in c.split(":"))
     try:
         p = rs.Pipeline(spec["stages"], spec["agg"], strategy=a.strategy, queue_cap=q, q0_stage=s, signal_cap=sc,
-                        flags=rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING | a.flags, chunk=a.chunk)
+                        flags=rs.RS_FLAG_STATS | rs.RS_FLAG_TIMING | a.flags, chunk=a.chunk, tag_from=a.tag_from)
         out = p.alloc_outputs(R, dev)
         ws = p.alloc_workspace(R, vals.numel(), dev)
         for _ in range(3):
