@@ -91,6 +91,13 @@ typedef enum {
     RS_OP_SUM_F32 = 21,      /* elem f32: v0 = float sum (fp32 accumulation)               */
     RS_OP_COUNT_MIN_U32 = 22,/* elem u32: v0 = uint32 count, v1 = uint32 min (0xFFFFFFFF if none) */
     RS_OP_COUNT_XOR64 = 23,  /* elem u8 : v0 = uint64 count, v1 = uint64 xor of mix64(i<<8|byte) */
+    RS_OP_SUM_I64_DROPS = 27,/* elem i32: v0 = int64 sum (as SUM_I64), v1 = uint64 number of items
+                                the FIRST stage dropped in the region.  The first stage counts them
+                                and announces the count with a signal of its own just before End
+                                ("a node ... may also generate additional signals");
+                                later stages forward it in stream position with the credit
+                                protocol and the aggregate records it.  Signal strategy; the first
+                                stage must not be the fused aggregate (2+ stages, or RS_FLAG_UNFUSED). */
     /* EMIT ops */
     RS_OP_EMIT_VALUE = 24,   /* elem i32/u32/f32: emit (value bits, region id) of each item   */
     RS_OP_EMIT_PAIR = 25     /* elem u8 (taxi stage 2): each surviving byte that

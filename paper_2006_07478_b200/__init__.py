@@ -21,7 +21,7 @@ RS_OK, RS_ERR_INVALID_ARG, RS_ERR_INVALID_TOPOLOGY, RS_ERR_UNSUPPORTED = 0, -1, 
 RS_ERR_WORKSPACE, RS_ERR_CUDA, RS_ERR_PROTOCOL, RS_ERR_NCCL = -4, -5, -6, -7
 RS_NODE_ENUMERATE, RS_NODE_FILTER, RS_NODE_TRANSFORM, RS_NODE_AGGREGATE, RS_NODE_EMIT, RS_NODE_SPLIT = 1, 2, 3, 4, 5, 6
 OPS = {"none": 0, "hash_lt": 1, "lt_u32": 2, "class": 3, "parent_lt": 4, "scale_f32": 10, "affine_i32": 11,
-       "sum_i64": 20, "sum_f32": 21, "count_min_u32": 22, "count_xor64": 23, "emit_value": 24, "emit_pair": 25}
+       "sum_i64": 20, "sum_f32": 21, "count_min_u32": 22, "count_xor64": 23, "emit_value": 24, "emit_pair": 25, "sum_i64_drops": 27}
 DTYPES = {"i32": 0, "u32": 1, "u8": 2, "f32": 3}
 STRATEGIES = {"signal": 0, "tagged": 1, "auto": 2, "context": 3, "hybrid": 4}
 STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
@@ -147,7 +147,7 @@ def _node(spec) -> tuple:
     raise ValueError(f"unknown stage {name}")
 
 
-AGG_ELEM = {"split_sum_i64": "i32", "sum_i64": "i32", "sum_f32": "f32", "count_min_u32": "u32", "count_xor64": "u8", "emit_value": "i32",
+AGG_ELEM = {"split_sum_i64": "i32", "sum_i64_drops": "i32", "sum_i64": "i32", "sum_f32": "f32", "count_min_u32": "u32", "count_xor64": "u8", "emit_value": "i32",
             "emit_pair": "u8"}
 
 
@@ -229,7 +229,7 @@ class Pipeline:
         import torch
         if self.agg == "sum_i64":
             return torch.empty(n_regions, dtype=torch.int64, device=device), None
-        if self.agg == "split_sum_i64":
+        if self.agg in ("split_sum_i64", "sum_i64_drops"):
             return (torch.empty(n_regions, dtype=torch.int64, device=device),
                     torch.empty(n_regions, dtype=torch.int64, device=device))
         if self.agg == "sum_f32":

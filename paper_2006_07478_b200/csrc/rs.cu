@@ -113,6 +113,7 @@ bool get_launch(const rs_pipeline *p, Launch *L) {
         case RS_OP_SUM_I64: *L = launch_agg20(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
         case RS_OP_SUM_F32: *L = launch_agg21(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
         case RS_OP_COUNT_MIN_U32: *L = launch_agg22(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
+        case RS_OP_SUM_I64_DROPS: *L = launch_agg27(p->nst, false, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, false); return true;
         case RS_OP_EMIT_PAIR: *L = launch_agg25(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, false); return true;
         case RS_OP_EMIT_VALUE: *L = launch_agg24(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
         case RS_OP_COUNT_XOR64: *L = launch_agg23(p->nst, p->cfg.strategy == RS_STRATEGY_TAGGED, (p->cfg.flags & RS_FLAG_UNFUSED) == 0, p->cfg.queue_cap, p->cfg.signal_cap, p->cfg.q0_stage, p->cfg.strategy == RS_STRATEGY_CONTEXT); return true;
@@ -247,6 +248,14 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
         case RS_OP_COUNT_MIN_U32: if (elem != RS_U32) return fail(RS_ERR_UNSUPPORTED, "COUNT_MIN_U32 needs u32 elements"); break;
         case RS_OP_COUNT_XOR64:
             if (elem != RS_U8) return fail(RS_ERR_UNSUPPORTED, "COUNT_XOR64 needs u8 elements");
+            break;
+        case RS_OP_SUM_I64_DROPS:
+            if (elem != RS_I32) return fail(RS_ERR_UNSUPPORTED, "SUM_I64_DROPS needs i32 elements");
+            if (cfg.strategy != RS_STRATEGY_SIGNAL || (cfg.flags & (RS_FLAG_TRACE | RS_FLAG_PROFILE)))
+                return fail(RS_ERR_UNSUPPORTED, "SUM_I64_DROPS is built for the signal strategy");
+            if (nst < ((cfg.flags & RS_FLAG_UNFUSED) ? 1 : 2))
+                return fail(RS_ERR_UNSUPPORTED, "SUM_I64_DROPS needs a first stage that is not the (fused) aggregate: "
+                                                "2+ stages, or 1+ with RS_FLAG_UNFUSED");
             break;
         case RS_OP_EMIT_PAIR:
             if (elem != RS_U8) return fail(RS_ERR_UNSUPPORTED, "EMIT_PAIR needs u8 elements");

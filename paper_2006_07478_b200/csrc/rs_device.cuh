@@ -272,6 +272,15 @@ struct AggT<26> {
     static constexpr int bytes0 = 8, bytes1 = 8;
 };   // RS_OP_EMIT_PAIR: element-wise exit of parsed "{x,y}" pairs (u8)
 
+// SUM_I64 plus a per-region count carried by a node-generated signal
+// (RS_OP_SUM_I64_DROPS): x = the int64 sum of the survivors, y = the items the
+// first stage dropped (added by lane 0 when the signal arrives).
+template <>
+struct AggT<27> : AggT<26> {
+    __device__ static A lift(uint32_t v) { return make_ulonglong2((unsigned long long)(long long)(int)v, 0ull); }
+    __device__ static A lift_i(uint32_t v, long long) { return lift(v); }
+};
+
 template <class AT>
 __device__ __forceinline__ typename AT::A warp_reduce(typename AT::A a) {
 #pragma unroll

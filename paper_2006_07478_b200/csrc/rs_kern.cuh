@@ -41,6 +41,8 @@ constexpr int W = 128;              // ensemble capacity (items)
 constexpr int IPL = W / 32;         // items per lane per ensemble
 constexpr uint32_t SLOT = 0x80000000u;  // key bit: partial-aggregate slot instead of region id
 constexpr uint32_t END_BIT = 0x80000000u;  // signal word: kind End
+constexpr uint32_t USER_BIT = 0x40000000u; // signal word: a node-generated (user) signal, payload in .x
+constexpr uint32_t CREDIT_MASK = 0x3fffffffu;   // signal word: the credit
 constexpr int MAXK = 4;             // max FILTER/TRANSFORM stages
 // RS_STRATEGY_AUTO crossover (children per region at which signal beats
 // tagged) by stage count 0..4, measured on B200 (tools/crossover.py)
@@ -233,6 +235,8 @@ Launch launch_agg20_hybrid(int K, bool fuse, int hyb, uint32_t qcap, uint32_t sc
 Launch launch_agg25_hybrid(int K, bool fuse, int hyb, uint32_t qcap, uint32_t scap, uint32_t sblk);
 // fan-out (SPLIT + two leaf SUM_I64 aggregates; rs_k26.cu), K <= 2 stages before the split
 Launch launch_agg26_split(int K, uint32_t qcap, uint32_t scap, uint32_t sblk);
+// SUM_I64 + stage-1 drop counts delivered by a node-generated signal (rs_k27.cu)
+Launch launch_agg27(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
 
 #ifndef RS_HOST_ONLY
 // Hybrid kernels: K stages, edges >= hyb tagged (1 <= hyb <= the aggregating
@@ -342,7 +346,7 @@ uint32_t smem_for(int K, uint32_t qcap, uint32_t scap, uint32_t ring) {
 template <int AGG>
 Launch launch_for(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx = false) {
     Launch L;
-    if constexpr (AGG != 23 && AGG != 24 && AGG != 25) {      // per-lane context strategy: 4-byte (in-place) element streams
+    if constexpr (AGG != 23 && AGG != 24 && AGG != 25 && AGG != 27) {      // per-lane context strategy: 4-byte (in-place) element streams
         if (ctx) {
             L = launch_for<AGG>(K, false, fuse, qcap, scap, sblk, false);
             L.main = fuse ? pick_k<AGG, false, true, true>(K) : pick_k<AGG, false, false, true>(K);

@@ -500,6 +500,10 @@ struct Pipe {
     uint32_t fkept;    // fused aggregate: items that reached it (per lane; node statistics)
     uint32_t ekey = 0; // EMIT, signal strategy: key of the open region
     uint32_t ckey = 0; // hybrid converter node: key of the open region
+    // RS_OP_SUM_I64_DROPS: stage 1 counts the items it drops per region part and
+    // announces the count with a signal of its own just before End
+    static constexpr bool UDROP = (AGG == 27);
+    uint32_t udrop = 0;
     long long base0, offR, off0;
     uint32_t nchunks;
     uint32_t q_start[K + 1 + NLQ]; // initial queue positions (edge 0 may start at the chunk-0 pad)
@@ -704,9 +708,10 @@ struct Pipe {
     // Sender rule for one signal on edge e: S empty -> |Q|;
     // otherwise items emitted since the tail signal.  Resets the counter.
     template <int e>
-    __device__ __forceinline__ void push_signal(uint32_t key, bool end, uint32_t credit_rule2) {
+    // kind: 0 (Begin), END_BIT, or USER_BIT (a node-generated signal, payload `key`)
+    __device__ __forceinline__ void push_signal(uint32_t key, uint32_t kind, uint32_t credit_rule2) {
         const uint32_t credit = (E<e>().sh == E<e>().st) ? (E<e>().qt - E<e>().qh) : credit_rule2;
-        if (lane == 0) S<e>()[E<e>().st & smask] = make_uint2(key, credit | (end ? END_BIT : 0u));
+        if (lane == 0) S<e>()[E<e>().st & smask] = make_uint2(key, credit | kind);
         E<e>().st += 1;
         E<e>().sent = 0;
     }
@@ -829,7 +834,7 @@ struct Pipe {
                 if (!begun) {
                     if (scap - (E<0>().st - E<0>().sh) == 0) return prog;
                     if constexpr (CTX) push_ctx<0>(key0, E<0>().qt - q_start[0]);
-                    else push_signal<0>(key0, false, E<0>().sent);
+                    else push_signal<0>(key0, 0u, E<0>().sent);
                     begun = true;
                     did = true;
                 }
@@ -845,7 +850,7 @@ struct Pipe {
                 if (k == cnt0) { pidx++; begun = false; did = true; }
             } else if constexpr (!TAG) {
                 if (k == cnt0 && scap - (E<0>().st - E<0>().sh) > 0) {
-                    push_signal<0>(key0, true, E<0>().sent);
+                    push_signal<0>(key0, END_BIT, E<0>().sent);
                     pidx++;
                     begun = false;
                     did = true;
@@ -905,7 +910,7 @@ struct Pipe {
         const uint32_t ql = E<e>().qt - E<e>().qh;
         if (!spend) return ql;
         if (E<e>().cur == 0 && !E<e>().xfer) {
-            const uint32_t c = S<e>()[E<e>().sh & smask].y & ~END_BIT;
+            const uint32_t c = S<e>()[E<e>().sh & smask].y & CREDIT_MASK;
             if (c > 0) { E<e>().cur = c; E<e>().xfer = true; }
         }
         return min(ql, E<e>().cur);
@@ -916,6 +921,7 @@ struct Pipe {
                                                 uint32_t nens, const Op op) {
         const uint32_t tl = filter_batch<TGE<n - 1>, Op, U8 && n == 1>(in, tin, imask, h, nens, Q<n>(), T<n>(), qm<n>(),
                                                                       E<n>().qt, op, lt, P.C - 1);
+        if constexpr (UDROP && n == 1) udrop += nens * W - (tl - E<n>().qt);
         if constexpr (HYB > 0 && n == HYB) stamp_tags<n>(E<n>().qt, tl);
         E<n>().sent += tl - E<n>().qt;
         E<n>().qt = tl;
@@ -1206,13 +1212,37 @@ struct Pipe {
             uint32_t nsig = 0;
             for (;;) {
                 if constexpr (!AGGN && !TGE<n>) {
-                    if (scap - (E<n>().st - E<n>().sh) == 0) break;   // output signal queue full
+                    // (the drop-count generator may push two signals: its own, then End)
+                    if (scap - (E<n>().st - E<n>().sh) < ((UDROP && n == 1) ? 2u : 1u)) break;   // output signal queue full
                 }
                 const uint2 hs = S<ei>()[E<ei>().sh & smask];
                 E<ei>().sh++;
                 E<ei>().xfer = false;
                 ++nsig;
                 const bool is_end = (hs.y & END_BIT) != 0;
+                if constexpr (UDROP) {
+                    if (hs.y & USER_BIT) {                // a node-generated signal
+                        if constexpr (AGGN) {
+                            if (lane == 0) acc.y += hs.x;  // the aggregate records the payload
+                        } else {
+                            push_signal<n>(hs.x, USER_BIT, E<n>().sent);   // forwarded in stream position
+                        }
+                        if (E<ei>().sh == E<ei>().st) break;
+                        const uint32_t c2 = S<ei>()[E<ei>().sh & smask].y & CREDIT_MASK;
+                        if (c2 > 0) {
+                            E<ei>().cur = c2;
+                            E<ei>().xfer = true;
+                            break;
+                        }
+                        continue;
+                    }
+                    if constexpr (n == 1 && !AGGN) {
+                        // stage 1 generates a signal of its own before forwarding End:
+                        // the items it dropped in this region (part)
+                        if (!is_end) udrop = 0;
+                        else push_signal<n>(udrop, USER_BIT, E<n>().sent);
+                    }
+                }
                 if constexpr (TR) if (P.trace) trace_event(n, is_end ? TR_END : TR_BEGIN, hs.x, 0u, 0u, 0u);
                 if constexpr (n <= K) {
                     if (!is_end && P.st[n - 1].op == RS_OP_PARENT_LT) set_pv(n, hs.x);
@@ -1231,10 +1261,10 @@ struct Pipe {
                 } else if constexpr (TGE<n>) {
                     if (!is_end) ckey = hs.x;    // hybrid converter: outputs carry this key as their tag
                 } else {
-                    push_signal<n>(hs.x, is_end, E<n>().sent);   // forwarded with a fresh credit
+                    push_signal<n>(hs.x, is_end ? END_BIT : 0u, E<n>().sent);   // forwarded with a fresh credit
                 }
                 if (E<ei>().sh == E<ei>().st) break;
-                const uint32_t c = S<ei>()[E<ei>().sh & smask].y & ~END_BIT;
+                const uint32_t c = S<ei>()[E<ei>().sh & smask].y & CREDIT_MASK;
                 if (c > 0) {
                     E<ei>().cur = c;
                     E<ei>().xfer = true;
@@ -1462,10 +1492,10 @@ struct Pipe {
                 ++nsig;
                 const bool is_end = (hs.y & END_BIT) != 0;
                 if (!is_end && P.st[K].op == RS_OP_PARENT_LT) set_pv(n, hs.x);
-                push_signal<ea>(hs.x, is_end, E<ea>().sent);     // each child: its own credit
-                push_signal<eb>(hs.x, is_end, E<eb>().sent);
+                push_signal<ea>(hs.x, is_end ? END_BIT : 0u, E<ea>().sent);     // each child: its own credit
+                push_signal<eb>(hs.x, is_end ? END_BIT : 0u, E<eb>().sent);
                 if (E<ei>().sh == E<ei>().st) break;
-                const uint32_t c = S<ei>()[E<ei>().sh & smask].y & ~END_BIT;
+                const uint32_t c = S<ei>()[E<ei>().sh & smask].y & CREDIT_MASK;
                 if (c > 0) {
                     E<ei>().cur = c;
                     E<ei>().xfer = true;
@@ -1528,7 +1558,7 @@ struct Pipe {
                 }
                 la = 0;                               // a::begin / after a::end
                 if (E<e>().sh == E<e>().st) break;
-                const uint32_t c = S<e>()[E<e>().sh & smask].y & ~END_BIT;
+                const uint32_t c = S<e>()[E<e>().sh & smask].y & CREDIT_MASK;
                 if (c > 0) {
                     E<e>().cur = c;
                     E<e>().xfer = true;
@@ -1865,6 +1895,7 @@ struct Pipe {
                                                                            qm<n>(), tl, lt, P.C - 1);
             });
             if constexpr (HYB > 0 && n == HYB) stamp_tags<n>(E<n>().qt, tl);
+            if constexpr (UDROP && n == 1) udrop += e - (tl - E<n>().qt);
             E<n>().sent += tl - E<n>().qt;
             E<n>().qt = tl;
         }

@@ -656,3 +656,27 @@ def test_tree_rejected_shapes(rs):
         rs.Pipeline(synth.sweep_stages(3), "split_sum_i64", split=("hash_lt", 3, 100))   # > 2 stages before SPLIT
     with pytest.raises(rs.RSError):
         rs.Pipeline([], "split_sum_i64", split=("hash_lt", 3, 100), strategy="tagged")
+
+
+@pytest.mark.parametrize("mode,nst", [("seq", 2), ("seq", 3), ("unfused", 1), ("unfused", 3)])
+def test_node_generated_signal(rs, mode, nst):
+    """A node-generated signal ("a node ... may also
+    generate additional signals"): the first stage counts the items it drops
+    in each region and announces the count with a signal of its own just
+    before End; the later stages forward it in stream position (credits) and
+    the aggregate records it.  v0 = the oracle's sums, v1 = items reaching
+    stage 1 minus items leaving it (oracle node counts), per region, with
+    regions split across chunks (parts add up in the fixup) and empty ones."""
+    lens = synth.lengths(3000, "zipf", seed=nst + 11, zipf_max=7000)
+    lens[::5] = 0
+    off = synth.offsets(lens, base=2)
+    vals = synth.values(int(off[-1]) + 1, "i32", seed=nst)
+    stages = synth.sweep_stages(nst)
+    ref = oracle.brute(vals, off, stages, "sum_i64")[0]
+    kc = oracle.node_counts(vals, off, stages)
+    drops = kc[:, 0] - kc[:, 1]
+    for cfg in (dict(chunk=2048), dict(chunk=4096, signal_cap=4, queue_cap=512, q0_stage=128, grid=3)):
+        got, st, p = run_gpu(rs, vals, off, stages, "sum_i64_drops", "signal", mode, **cfg)
+        np.testing.assert_array_equal(got[0], ref)
+        np.testing.assert_array_equal(got[1], drops)
+        assert st[2][3] == st[1][3] + st[1][3] // 2       # node 2 consumes Begin, End and the new signal per part
