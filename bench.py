@@ -240,8 +240,9 @@ def run_reference(args):
         if not torch.cuda.is_available():
             raise RuntimeError("no GPU")
         vals, off = make_inputs(spec, seed=0x5EED + 2, device=torch.device("cuda", 0))
-        # the bounded sample: a prefix of ~2^25 children of the very same stream
-        r = _prefix(off.cpu().numpy(), 1 << 25)
+        # the bounded sample: a prefix of up to ~2^28 children of the very same stream
+        # (each step times the interpreter on as much of it as ~20 s / steps allows)
+        r = _prefix(off.cpu().numpy(), 1 << 28)
         oh = off[:r + 1].cpu().numpy()
         vh = vals[: int(oh[-1])].cpu().numpy()
         del vals, off
