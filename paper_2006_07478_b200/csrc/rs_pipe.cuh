@@ -894,6 +894,8 @@ struct Pipe {
         }
     }
     __device__ __forceinline__ void write_tags_uniform(uint32_t key, uint32_t k) {
+        // (not unrolled: the instruction cache is the tagged kernel's binding limit)
+#pragma unroll 1
         for (uint32_t i = lane; i < k; i += 32) T<0>()[(E<0>().qt + i) & (ring0 - 1)] = key;
     }
 
@@ -1912,7 +1914,35 @@ struct Pipe {
     template <class Op>
     __device__ __forceinline__ void agg_tagged_fold(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                                     uint32_t e, const Op op) {
+        // fast path, unrolled: a full ensemble that continues the carry region
+        // (the common case for long regions) folds without the segmented scan
+        if (e == (uint32_t)W && akey != 0xffffffffu) {
+            bool same = true;
 #pragma unroll
+            for (int j = 0; j < IPL; ++j) same = same && tin[(h + j * 32 + lane) & imask] == akey;
+            if (__all_sync(kFull, same)) {
+                if constexpr (U8) {
+                    if (__any_sync(kFull, dkey != akey)) {
+                        adelta = part_delta(akey);
+                        dkey = akey;
+                    }
+                }
+                A part = AT::id();
+#pragma unroll
+                for (int j = 0; j < IPL; ++j) {
+                    uint32_t x = agg_load(in, h + j * 32 + lane, imask);
+                    const bool keep = op(x);
+                    if constexpr (NA) fkept += keep ? 1u : 0u;
+                    if (keep) part = AT::comb(part, AT::lift_i(x, adelta));
+                }
+                acc = AT::comb(acc, part);
+                return;
+            }
+        }
+        // ensembles with region changes: one slice per iteration, not unrolled -- the
+        // segmented fold is large and the tagged kernel is instruction-cache bound
+        // (profiles/r2_k_pipeline_full_zipf_tagged.txt)
+#pragma unroll 1
         for (int j = 0; j < IPL; ++j) {
             const int cntj = (int)e - j * 32;
             if (cntj <= 0) break;
