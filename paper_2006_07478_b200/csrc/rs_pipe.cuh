@@ -183,25 +183,25 @@ __device__ __noinline__ uint32_t partial_stage(const Op op, const uint32_t *in, 
         __syncwarp();
         return tl;
     }
+    // One slice per iteration, not unrolled (the instruction cache binds; a
+    // partial ensemble is rarer than a full one).  In-place rings: slice j's
+    // stores land below tl + 32(j+1) <= h + 32(j+1), i.e. below every later
+    // slice's reads; within a slice every lane reads before any lane stores.
     const uint32_t lane = threadIdx.x & 31u;
-    uint32_t v[IPL], tg[IPL];
-#pragma unroll
-    for (int j = 0; j < IPL; ++j) {
+#pragma unroll 1
+    for (uint32_t j = 0; j * 32u < e; ++j) {
         const uint32_t idx = j * 32 + lane;
         const bool act = idx < e;
-        v[j] = act ? load_item<U8IN>(in, h + idx, imask, cmask) : 0u;
-        if constexpr (TAG) tg[j] = act ? tin[(h + idx) & imask] : 0u;
-    }
-    __syncwarp();   // in-place rings: all reads before any compaction store
-#pragma unroll
-    for (int j = 0; j < IPL; ++j) {
-        if ((uint32_t)j * 32u >= e) break;
-        const bool keep = (j * 32 + lane) < e && op(v[j]);
+        uint32_t v = act ? load_item<U8IN>(in, h + idx, imask, cmask) : 0u;
+        uint32_t tg = 0;
+        if constexpr (TAG) tg = act ? tin[(h + idx) & imask] : 0u;
+        __syncwarp();
+        const bool keep = act && op(v);
         const uint32_t mk = __ballot_sync(kFull, keep);   // stable compaction
         if (keep) {
             const uint32_t pos = (tl + __popc(mk & lt)) & qmask;
-            out[pos] = v[j];
-            if constexpr (TAG) tout[pos] = tg[j];
+            out[pos] = v;
+            if constexpr (TAG) tout[pos] = tg;
         }
         tl += __popc(mk);
     }
@@ -279,25 +279,21 @@ __device__ __noinline__ FusedAcc<AT> fused_batch(const uint32_t *in, uint32_t im
 // written, so overlapping source and destination are safe).
 template <bool TAG>
 __device__ __noinline__ void move_items(uint32_t *q, uint32_t *tq, uint32_t end, uint32_t n, uint32_t shift, uint32_t m) {
+    // 32-item slices, highest first, not unrolled (code size): a slice's
+    // stores land at or above its own reads and above every lower slice
     const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll 1
     while (n > 0) {
-        const uint32_t c = n < (uint32_t)W ? n : (uint32_t)W;
+        const uint32_t c = n < 32u ? n : 32u;
         const uint32_t s0 = end - c;
-        uint32_t v[IPL], tg[IPL];
-#pragma unroll
-        for (int j = 0; j < IPL; ++j) {
-            const uint32_t idx = 32 * j + lane;
-            v[j] = idx < c ? q[(s0 + idx) & m] : 0u;
-            if constexpr (TAG) tg[j] = idx < c ? tq[(s0 + idx) & m] : 0u;
-        }
+        const bool act = lane < c;
+        const uint32_t v = act ? q[(s0 + lane) & m] : 0u;
+        uint32_t tg = 0;
+        if constexpr (TAG) tg = act ? tq[(s0 + lane) & m] : 0u;
         __syncwarp();
-#pragma unroll
-        for (int j = 0; j < IPL; ++j) {
-            const uint32_t idx = 32 * j + lane;
-            if (idx < c) {
-                q[(s0 + shift + idx) & m] = v[j];
-                if constexpr (TAG) tq[(s0 + shift + idx) & m] = tg[j];
-            }
+        if (act) {
+            q[(s0 + shift + lane) & m] = v;
+            if constexpr (TAG) tq[(s0 + shift + lane) & m] = tg;
         }
         __syncwarp();
         end -= c;
@@ -322,7 +318,7 @@ __device__ __noinline__ FusedAcc<AT> fused_partial(const uint32_t *in, uint32_t 
         st.kept += __popc(km);
         st.acc = fold_kept<AT>(st.acc, v, km, adelta);
     } else {
-#pragma unroll
+#pragma unroll 1
         for (int j = 0; j < IPL; ++j) {
             if ((uint32_t)j * 32u >= e) break;
             const uint32_t idx = j * 32 + lane;
