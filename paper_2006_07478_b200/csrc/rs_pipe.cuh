@@ -485,7 +485,7 @@ struct Pipe {
     // part-info cache: lane i holds part pc_base + i of F0
     uint32_t pc_base;
     bool pc_valid;
-    long long pc_ps, pc_pe;
+    uint32_t pc_ps, pc_pe;         // part bounds relative to F0.beg (a chunk spans < 2^31 elements)
     uint32_t pc_key;
     // aggregate state
     A acc;             // per-lane partial accumulator
@@ -669,21 +669,24 @@ struct Pipe {
     // ------------------------------------------------------ enumerate
     // Part qi of chunk F0: [start, end) elements and its key (region id, or a
     // partial slot for the chunk's head part / a tail part crossing the chunk end).
-    __device__ __forceinline__ void part_info(uint32_t qi, bool valid, long long &ps, long long &pe, uint32_t &key) const {
-        ps = pe = F0.end;
+    // Part bounds are returned relative to F0.beg (32-bit: the enumerate loop's
+    // scans, shuffles and compares then stay 32-bit -- smaller code).
+    __device__ __forceinline__ void part_info(uint32_t qi, bool valid, uint32_t &ps, uint32_t &pe, uint32_t &key) const {
+        const uint32_t len = flen(F0);
+        ps = pe = len;
         key = 0;
         if (!valid) return;
         if (F0.head && qi == 0) {
-            ps = F0.beg;
+            ps = 0;
             const long long e = P.off[F0.fr0];
-            pe = e < F0.end ? e : F0.end;
+            pe = e < F0.end ? (uint32_t)(e - F0.beg) : len;
             key = SLOT | (uint32_t)(2 * F0.k);
         } else {
             const uint32_t r = F0.fr0 + qi - (F0.head ? 1u : 0u);
-            ps = P.off[r];
+            ps = (uint32_t)(P.off[r] - F0.beg);
             const long long e = P.off[r + 1];
-            if (e > F0.end) { pe = F0.end; key = SLOT | (uint32_t)(2 * F0.k + 1); }
-            else { pe = e; key = r; }
+            if (e > F0.end) { pe = len; key = SLOT | (uint32_t)(2 * F0.k + 1); }
+            else { pe = (uint32_t)(e - F0.beg); key = r; }
         }
     }
 
@@ -748,11 +751,11 @@ struct Pipe {
                 part_info(pidx + lane, pidx + lane < np, pc_ps, pc_pe, pc_key);
             }
             const uint32_t d = pidx - pc_base;
-            const long long e_next = F0.beg + (long long)(E<0>().qt - F0.pos);
+            const uint32_t e_next = E<0>().qt - F0.pos;              // next element, relative to F0.beg
             if (TAG || begun) {
                 // long part in progress: stream the staged items without the per-part scan
-                const long long pe0 = __shfl_sync(kFull, pc_pe, d);
-                if (pe0 - e_next > (long long)avail) {
+                const uint32_t pe0 = __shfl_sync(kFull, pc_pe, d);
+                if ((int)(pe0 - e_next) > (int)avail) {
                     if (avail == 0) return prog;
                     if constexpr (TAG) write_tags_uniform(__shfl_sync(kFull, pc_key, d), avail);
                     E<0>().qt += avail;
@@ -761,13 +764,13 @@ struct Pipe {
                     return true;
                 }
             }
-            long long ps = __shfl_down_sync(kFull, pc_ps, d);
-            long long pe = __shfl_down_sync(kFull, pc_pe, d);
+            uint32_t ps = __shfl_down_sync(kFull, pc_ps, d);
+            uint32_t pe = __shfl_down_sync(kFull, pc_pe, d);
             uint32_t key = __shfl_down_sync(kFull, pc_key, d);
             const bool valid = (lane + d < 32) && (pidx + lane < np);
-            if (!valid) ps = pe = F0.end;
+            if (!valid) ps = pe = flen(F0);
             if (lane == 0 && ps < e_next) ps = e_next;     // resume inside part pidx
-            const uint32_t cnt = (uint32_t)(pe - ps);
+            const uint32_t cnt = pe - ps;
             uint32_t cum = cnt;
             const uint32_t sig = TAG ? 0u : ((lane == 0 && begun) ? (CTX ? 0u : 1u) : (CTX ? 1u : 2u));
             uint32_t scum = sig;
