@@ -170,14 +170,26 @@ __device__ __noinline__ uint32_t filter_batch(const uint32_t *in, const uint32_t
     return tl;
 }
 
+// In-place rings without tags (the signal strategy's stage nodes): input and
+// output queue share one ring and mask -- the same loops with fewer call
+// arguments to marshal at every firing (instruction-cache footprint).
+template <class Op>
+__device__ __noinline__ uint32_t filter_batch_ip(uint32_t *ring, uint32_t mask, uint32_t h, uint32_t nens, uint32_t tl,
+                                                 const Op op) {
+    const uint32_t lt = lanemask_lt();
+    for (uint32_t k = 0; k < nens; ++k, h += W) filter_slices<false, IPL, Op, false>(ring, nullptr, mask, h, ring, nullptr, mask, tl, op, lt, 0u);
+    __syncwarp();
+    return tl;
+}
+
 // One partial ensemble (e < w items: signal-bounded or the drained tail) of
 // a FILTER/TRANSFORM node, specialised per op like the full ensembles and
 // shared by every stage node (code size); only the ceil(e/32) occupied
 // slices are visited (e is warp-uniform).
 template <bool TAG, class Op, bool U8IN>
-__device__ __noinline__ uint32_t partial_stage(const Op op, const uint32_t *in, const uint32_t *tin,
-                                               uint32_t imask, uint32_t h, uint32_t e, uint32_t *out, uint32_t *tout,
-                                               uint32_t qmask, uint32_t tl, uint32_t lt, uint32_t cmask) {
+__device__ __forceinline__ uint32_t partial_body(const Op op, const uint32_t *in, const uint32_t *tin,
+                                                 uint32_t imask, uint32_t h, uint32_t e, uint32_t *out, uint32_t *tout,
+                                                 uint32_t qmask, uint32_t tl, uint32_t lt, uint32_t cmask) {
     if constexpr (!TAG && U8IN && std::is_same<Op, OpClass1>::value) {
         tl = swar_filter(in, imask, h, e, out, qmask, tl, op, lt, cmask);
         __syncwarp();
@@ -207,6 +219,18 @@ __device__ __noinline__ uint32_t partial_stage(const Op op, const uint32_t *in, 
     }
     __syncwarp();
     return tl;
+}
+
+template <bool TAG, class Op, bool U8IN>
+__device__ __noinline__ uint32_t partial_stage(const Op op, const uint32_t *in, const uint32_t *tin,
+                                               uint32_t imask, uint32_t h, uint32_t e, uint32_t *out, uint32_t *tout,
+                                               uint32_t qmask, uint32_t tl, uint32_t lt, uint32_t cmask) {
+    return partial_body<TAG, Op, U8IN>(op, in, tin, imask, h, e, out, tout, qmask, tl, lt, cmask);
+}
+template <class Op>
+__device__ __noinline__ uint32_t partial_stage_ip(const Op op, uint32_t *ring, uint32_t mask, uint32_t h, uint32_t e,
+                                                  uint32_t tl) {
+    return partial_body<false, Op, false>(op, ring, nullptr, mask, h, e, ring, nullptr, mask, tl, lanemask_lt(), 0u);
 }
 
 // Fused terminal node, full ensembles, signal strategy (see Pipe::FUSE): the
@@ -920,8 +944,10 @@ struct Pipe {
     template <int n, class Op>
     __device__ __forceinline__ void filter_full(const uint32_t *in, const uint32_t *tin, uint32_t imask, uint32_t h,
                                                 uint32_t nens, const Op op) {
-        const uint32_t tl = filter_batch<TGE<n - 1>, Op, U8 && n == 1>(in, tin, imask, h, nens, Q<n>(), T<n>(), qm<n>(),
-                                                                      E<n>().qt, op, lt, P.C - 1);
+        uint32_t tl;
+        if constexpr (INPLACE && !TAGANY) tl = filter_batch_ip(Q<0>(), ring0 - 1, h, nens, E<n>().qt, op);
+        else tl = filter_batch<TGE<n - 1>, Op, U8 && n == 1>(in, tin, imask, h, nens, Q<n>(), T<n>(), qm<n>(),
+                                                             E<n>().qt, op, lt, P.C - 1);
         if constexpr (UDROP && n == 1) udrop += nens * W - (tl - E<n>().qt);
         if constexpr (HYB > 0 && n == HYB) stamp_tags<n>(E<n>().qt, tl);
         E<n>().sent += tl - E<n>().qt;
@@ -1892,7 +1918,8 @@ struct Pipe {
         } else {
             uint32_t tl = E<n>().qt;
             with_op_k(P.st[n - 1], pvn(n), [&](auto op) {
-                tl = partial_stage<TGE<n - 1>, decltype(op), U8 && n == 1>(op, in, tin, imask, h, e, Q<n>(), T<n>(),
+                if constexpr (INPLACE && !TAGANY) tl = partial_stage_ip(op, Q<0>(), ring0 - 1, h, e, tl);
+                else tl = partial_stage<TGE<n - 1>, decltype(op), U8 && n == 1>(op, in, tin, imask, h, e, Q<n>(), T<n>(),
                                                                            qm<n>(), tl, lt, P.C - 1);
             });
             if constexpr (HYB > 0 && n == HYB) stamp_tags<n>(E<n>().qt, tl);
