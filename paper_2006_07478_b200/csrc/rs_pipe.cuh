@@ -170,18 +170,6 @@ __device__ __noinline__ uint32_t filter_batch(const uint32_t *in, const uint32_t
     return tl;
 }
 
-// In-place rings without tags (the signal strategy's stage nodes): input and
-// output queue share one ring and mask -- the same loops with fewer call
-// arguments to marshal at every firing (instruction-cache footprint).
-template <class Op>
-__device__ __noinline__ uint32_t filter_batch_ip(uint32_t *ring, uint32_t mask, uint32_t h, uint32_t nens, uint32_t tl,
-                                                 const Op op) {
-    const uint32_t lt = lanemask_lt();
-    for (uint32_t k = 0; k < nens; ++k, h += W) filter_slices<false, IPL, Op, false>(ring, nullptr, mask, h, ring, nullptr, mask, tl, op, lt, 0u);
-    __syncwarp();
-    return tl;
-}
-
 // One partial ensemble (e < w items: signal-bounded or the drained tail) of
 // a FILTER/TRANSFORM node, specialised per op like the full ensembles and
 // shared by every stage node (code size); only the ceil(e/32) occupied
@@ -232,6 +220,67 @@ __device__ __noinline__ uint32_t partial_stage_ip(const Op op, uint32_t *ring, u
                                                   uint32_t tl) {
     return partial_body<false, Op, false>(op, ring, nullptr, mask, h, e, ring, nullptr, mask, tl, lanemask_lt(), 0u);
 }
+
+// In-place rings without tags (the signal strategy's stage nodes): input and
+// output queue share one ring and mask -- the same loops with fewer call
+// arguments to marshal at every firing (instruction-cache footprint).
+// Ensembles whose input slots and outputs do not wrap the ring use linear
+// shared addresses: one LDS with an immediate offset per slice and an
+// LEA-formed store address (66 -> ~44 SASS per ensemble); an ensemble that
+// straddles the ring end takes the masked loop.
+template <class Op>
+__device__ __forceinline__ uint32_t filter_linear_ens(uint32_t si, uint32_t so, const Op &op, uint32_t lt) {
+    const uint32_t lane4 = (threadIdx.x & 31u) * 4u;
+    uint32_t v[IPL];
+#pragma unroll
+    for (int j = 0; j < IPL; ++j) v[j] = lds32(si + lane4 + 128u * j);
+    __syncwarp();      // every lane's reads before any compaction store
+    bool keep[IPL];
+    uint32_t mk[IPL], c[IPL];
+#pragma unroll
+    for (int j = 0; j < IPL; ++j) {
+        keep[j] = op(v[j]);
+        mk[j] = __ballot_sync(kFull, keep[j]);
+        c[j] = __popc(mk[j]);
+    }
+    uint32_t rel = 0;
+#pragma unroll
+    for (int j = 0; j < IPL; ++j) {
+        if (keep[j]) sts32(so + (rel + __popc(mk[j] & lt)) * 4u, v[j]);
+        rel += c[j];
+    }
+    return rel;
+}
+template <class Op>
+__device__ __noinline__ uint32_t filter_batch_ip(uint32_t *ring, uint32_t mask, uint32_t h, uint32_t nens, uint32_t tl,
+                                                 const Op op) {
+    const uint32_t lt = lanemask_lt();
+    const uint32_t rb = smem_addr(ring);
+    while (nens > 0) {
+        const uint32_t hi = h & mask, ti = tl & mask;
+        const uint32_t nl = min(nens, min((mask + 1 - hi) / W, (mask + 1 - ti) / W));
+        if (nl == 0) {      // the ensemble straddles the ring end: the (compact) masked loop
+            tl = partial_stage_ip(op, ring, mask, h, W, tl);
+            h += W;
+            --nens;
+            continue;
+        }
+        uint32_t si = rb + hi * 4u, so = rb + ti * 4u, n = 0;
+#pragma unroll 1
+        for (uint32_t k = 0; k < nl; ++k) {
+            const uint32_t c = filter_linear_ens(si, so, op, lt);
+            si += 4u * W;
+            so += 4u * c;
+            n += c;
+        }
+        h += nl * W;
+        tl += n;
+        nens -= nl;
+    }
+    __syncwarp();
+    return tl;
+}
+
 
 // Fused terminal node, full ensembles, signal strategy (see Pipe::FUSE): the
 // node's op decides each item, survivors are folded into the per-lane
