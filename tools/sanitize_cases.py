@@ -70,6 +70,24 @@ for L in (3, 100):
         if int(c.item()) != rv.size or p.check():
             bad += 1
             print("EMIT MISMATCH", strat)
+    # tree topology (SPLIT + two leaves) and the node-generated drop-count signal
+    for K in (0, 2):
+        st = synth.sweep_stages(K)
+        ra, rb = oracle.brute_split(vals, off, st, ("hash_lt", 0x27D4EB2F, 128))
+        p = rs.Pipeline(st, "split_sum_i64", split=("hash_lt", 0x27D4EB2F, 128), grid=2, chunk=2048, q0_stage=128)
+        got, code = run(p, vals, off)
+        nb = int((got[0] != ra).sum() + (got[1] != rb).sum())
+        bad += nb + (code != 0)
+        if nb or code:
+            print("TREE MISMATCH", L, K, nb, code)
+    st = synth.sweep_stages(2)
+    kc = oracle.node_counts(vals, off, st)
+    p = rs.Pipeline(st, "sum_i64_drops", grid=2, chunk=2048, q0_stage=128)
+    got, code = run(p, vals, off)
+    nb = int((got[0] != oracle.brute(vals, off, st, "sum_i64")[0]).sum() + (got[1] != kc[:, 0] - kc[:, 1]).sum())
+    bad += nb + (code != 0)
+    if nb or code:
+        print("DROPS MISMATCH", L, nb, code)
 # text (SWAR path) and the taxi parser
 b, off = synth.text(200000, seed=3, line_mean=300.0)
 for strat in ("signal", "tagged"):
