@@ -32,3 +32,5 @@ for wk in "sweep_var_L4096 signal k_pipelineILi3ELi20ELb0ELb1ELb0ELb0ELi0E" "zip
       > $O/summary_$1_$2.txt 2>&1
 done
 python bench.py > $O/bench.log 2>&1
+{ compute-sanitizer --tool memcheck --error-exitcode 0 python tools/sanitize_cases.py 2>&1 | tail -4;
+  compute-sanitizer --tool racecheck --racecheck-report hazard python tools/sanitize_cases.py 2>&1 | tail -4; } > $O/sanitizer.txt
