@@ -151,6 +151,20 @@ enum {
                                 largest item value), in order, so a host checker can verify
                                 bracketing, unmixed ensembles and per-bracket counts.  A
                                 separate kernel instantiation: no cost when off. */
+    RS_FLAG_SHORT_OFF = 128u,/* never use the short-region kernel (see RS_FLAG_SHORT_ON)  */
+    RS_FLAG_SHORT_ON = 256u, /* signal strategy, SUM_I64, fused aggregate, 1+ stages: always run
+                                the short-region kernel.  It fires the same ensembles and
+                                consumes the same signals in the same order as the general
+                                kernel (identical results and counters) but handles up to 32
+                                pending signals per node warp-parallel (one load, one store)
+                                with the partial ensembles they bound in between -- the regime of
+                                regions shorter than w.  Default (neither flag):
+                                when n_elems < 2w * n_regions both kernels are enqueued and the
+                                prepass picks the short-region one iff the call's children
+                                off[R] - off[0] < 96 * R (decided on the device, like AUTO;
+                                the crossover measured on B200).  Its default geometry is its
+                                own (a 16w ring, stages of 4w, signal queues of 128) unless
+                                queue_cap / signal_cap / q0_stage are set. */
     RS_FLAG_UNFUSED = 32u    /* sequential scheduler: keep the AGGREGATE as a separate node
                                 with its own queue (the paper's node structure).
                                 Default: the aggregate is folded into the last FILTER/

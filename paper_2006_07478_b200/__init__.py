@@ -27,6 +27,7 @@ STRATEGIES = {"signal": 0, "tagged": 1, "auto": 2, "context": 3, "hybrid": 4}
 STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
 RS_FLAG_STATS, RS_FLAG_VALIDATE, RS_FLAG_TIMING, RS_FLAG_RESERVED8, RS_FLAG_PROFILE, RS_FLAG_UNFUSED = 1, 2, 4, 8, 16, 32
 RS_FLAG_TRACE = 64
+RS_FLAG_SHORT_OFF, RS_FLAG_SHORT_ON = 128, 256
 TRACE_ENSEMBLE, TRACE_BEGIN, TRACE_END = 1, 2, 3
 
 EXPORTS = ["rs_config_default", "rs_pipeline_create", "rs_pipeline_workspace_bytes", "rs_pipeline_run",

@@ -52,6 +52,10 @@ struct rs_pipeline {
     uint32_t auto_min_len = 0;
     cudaStream_t last_stream = nullptr;
     bool has_parent = false;      // a PARENT_LT node reads d_parent_ctx
+    // short-region kernel geometry (RS_FLAG_SHORT_*): its own ring / stage /
+    // signal-queue sizes unless the caller fixed them
+    bool geom_default = false;
+    int sh_grid = 0, sh_wpb = 0;
     // RS_FLAG_TRACE event buffer (caller-owned device memory)
     void *trace = nullptr;
     uint64_t trace_bytes = 0;
@@ -350,6 +354,7 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
         return fail(RS_ERR_UNSUPPORTED, "q0_stage must be a power of 2 in [128, 4096]");
     if (cfg.chunk < cfg.q0_stage) return fail(RS_ERR_UNSUPPORTED, "chunk must be >= q0_stage");   // stages never straddle chunks
     rs_pipeline *p = new rs_pipeline();
+    p->geom_default = !cfg_in || (cfg_in->queue_cap == 0 && cfg_in->signal_cap == 0 && cfg_in->q0_stage == 0);
     p->cfg = cfg;
     p->elem = elem;
     p->n_nodes = n_nodes;
@@ -473,6 +478,7 @@ static rs_status prepare(rs_pipeline *p, const void *d_elems, int64_t n_elems, c
         p->wpb = best_w;
         p->grid = p->cfg.grid > 0 ? p->cfg.grid : sms * (best / best_w);
         p->device = dev;
+        p->sh_grid = 0;                   // re-sized on the next short-region launch
     }
     pr.cta_smem = L.inst_bytes * p->wpb;
 
@@ -556,6 +562,51 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
         Kpre.tagged = -1;
         Kpre.auto_min_len = p->auto_min_len;
     }
+    // short-region kernel (RS_FLAG_SHORT_ON / _OFF, rs.h).  Default geometry:
+    // a ring of 16w items in TMA stages of 4w and signal queues of 128 -- the
+    // kernel is latency-bound at short regions, and the smaller footprint fits
+    // 16 instances per SM (profiles/r2_tuning.txt)
+    Launch shl{};
+    Prep ps = pa;
+    if (!is_auto && p->agg == RS_OP_SUM_I64 && p->cfg.strategy == RS_STRATEGY_SIGNAL && p->nst >= 1 &&
+        !(p->cfg.flags & (RS_FLAG_UNFUSED | RS_FLAG_TRACE | RS_FLAG_PROFILE | RS_FLAG_SHORT_OFF)) &&
+        ((p->cfg.flags & RS_FLAG_SHORT_ON) || n_elems < 2ll * W * n_regions)) {
+        const uint32_t qc = p->geom_default ? 16 * W : p->cfg.queue_cap;
+        const uint32_t sc = p->geom_default ? 128 : p->cfg.signal_cap;
+        const uint32_t sb = p->geom_default ? 4 * W : p->cfg.q0_stage;
+        shl = short_launch_agg20(p->nst, qc, sc, sb);
+        if (shl.main) {
+            if (!ensure_smem_attr(shl.main, p->device)) return fail(RS_ERR_CUDA, "cannot raise the kernel's shared-memory limit");
+            if (p->sh_grid == 0) {
+                int best = 0, best_w = 1;
+                for (int w = WPB_MAX; w >= 1; --w) {
+                    int per_sm = 0;
+                    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, shl.main, w * 32, shl.inst_bytes * w) != cudaSuccess) {
+                        cudaGetLastError();
+                        continue;
+                    }
+                    if (per_sm * w > best) { best = per_sm * w; best_w = w; }
+                }
+                if (best < 1) return fail(RS_ERR_UNSUPPORTED, "short-region kernel does not fit on an SM");
+                int sms = 0;
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+                p->sh_wpb = best_w;
+                p->sh_grid = p->cfg.grid > 0 ? p->cfg.grid : sms * (best / best_w);
+            }
+            ps.K.qcap = qc;
+            ps.K.scap = sc;
+            ps.K.q0_stage = sb;
+            ps.K.ring0 = shl.ring0;
+            ps.cta_smem = shl.inst_bytes * p->sh_wpb;
+        }
+    }
+    KernelFn sh = shl.main;
+    const bool both = sh && !(p->cfg.flags & RS_FLAG_SHORT_ON);
+    if (both) {
+        Kpre.short_len = SHORT_LEN;
+        pa.K.short_sel = 1;
+        ps.K.short_sel = 2;
+    }
     if ((pa.K.flags & RS_FLAG_TRACE) && (!p->trace || p->trace_bytes < 64))
         return fail(RS_ERR_INVALID_ARG, "RS_FLAG_TRACE needs rs_pipeline_set_trace");
     if (pa.K.flags & RS_FLAG_TRACE) {
@@ -574,13 +625,15 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
     if (timing) cudaEventRecord(p->ev[0], stream);
     pa.L.pre<<<pre_blocks, 256, 0, stream>>>(Kpre);
     if (timing) cudaEventRecord(p->ev[1], stream);
-    pa.L.main<<<(is_auto ? p->sub[0] : p)->grid, (is_auto ? p->sub[0] : p)->wpb * 32, pa.cta_smem, stream>>>(pa.K);
+    if (!sh || both)
+        pa.L.main<<<(is_auto ? p->sub[0] : p)->grid, (is_auto ? p->sub[0] : p)->wpb * 32, pa.cta_smem, stream>>>(pa.K);
+    if (sh) sh<<<p->sh_grid, p->sh_wpb * 32, ps.cta_smem, stream>>>(ps.K);
     if (is_auto) pb.L.main<<<p->sub[1]->grid, p->sub[1]->wpb * 32, pb.cta_smem, stream>>>(pb.K);
     if (timing) cudaEventRecord(p->ev[2], stream);
     int fix_blocks = (int)std::min<long long>((pa.wl.max_chunks + 255) / 256, 148 * 8);
     pa.L.fix<<<std::max(fix_blocks, 1), 256, 0, stream>>>(pa.K);
     if (timing) cudaEventRecord(p->ev[3], stream);
-    p->launches = is_auto ? 4 : 3;
+    p->launches = (is_auto || both) ? 4 : 3;
     p->last_ws = d_ws;
     p->last_stream = stream;
     cudaError_t e = cudaGetLastError();

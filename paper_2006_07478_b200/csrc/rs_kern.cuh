@@ -47,6 +47,9 @@ constexpr int MAXK = 4;             // max FILTER/TRANSFORM stages
 // RS_STRATEGY_AUTO crossover (children per region at which signal beats
 // tagged) by stage count 0..4, measured on B200 (tools/crossover.py)
 constexpr uint32_t AUTO_T0 = 128, AUTO_T1 = 256, AUTO_T2 = 512, AUTO_T3 = 768, AUTO_T4 = 2048;
+// short-region kernel: chosen on the device iff the call's mean region length
+// is below this (children per region; measured on B200, profiles/r2_tuning.txt)
+constexpr uint32_t SHORT_LEN = 96;
 constexpr int NSTMAX = 8;           // TMA stages of an in-place ring (sequential kernel)
 constexpr int WPB = 4;              // warps (instances) per CTA (default)
 constexpr int WPB_MAX = 16;         // sequential kernel: up to 16 instances per CTA (one CTA may fill an SM)
@@ -67,6 +70,7 @@ struct WsHdr {
     int32_t err;         // first device error
     uint32_t nchunks;
     int32_t sel;         // strategy the run uses (0 signal, 1 tagged; RS_STRATEGY_AUTO decides on the device)
+    int32_t ssel;        // signal strategy: 1 = the short-region (SH) kernel runs, 0 = the general one
     long long base0;     // align_down(offsets[0], 16 bytes)
     long long off0, offR;
 };
@@ -91,6 +95,8 @@ struct KParams {
     int32_t tagged;                 // 1 tagged (or hybrid: the aggregate folds by tag); -1 = AUTO (the prepass decides)
     int32_t auto_sel;               // AUTO: 0 always run; 1 = run iff hdr->sel == 0; 2 = iff hdr->sel == 1
     uint32_t auto_min_len;          // AUTO: signal iff children >= auto_min_len * regions
+    int32_t short_sel;              // 0 always run; 1 = run iff hdr->ssel == 0; 2 = iff hdr->ssel == 1
+    uint32_t short_len;             // prepass: ssel = 1 iff children < short_len * regions
     int32_t nst;
     StageP st[MAXK];
     const uint32_t *ctx;            // parent context, one uint32 per region (PARENT_LT), or null
@@ -146,6 +152,7 @@ __global__ void k_prepass(KParams P) {
         if (bad) atomicCAS((int *)&P.hdr->err, 0, ERR_OFFSETS);
         P.hdr->nchunks = (uint32_t)nch;
         P.hdr->sel = tagged ? 1 : 0;
+        P.hdr->ssel = (double)(offR - off0) < (double)P.short_len * (double)P.R ? 1 : 0;
         P.hdr->base0 = base0;
         P.hdr->off0 = off0;
         P.hdr->offR = offR;
@@ -235,6 +242,10 @@ Launch launch_agg20_hybrid(int K, bool fuse, int hyb, uint32_t qcap, uint32_t sc
 Launch launch_agg25_hybrid(int K, bool fuse, int hyb, uint32_t qcap, uint32_t scap, uint32_t sblk);
 // fan-out (SPLIT + two leaf SUM_I64 aggregates; rs_k26.cu), K <= 2 stages before the split
 Launch launch_agg26_split(int K, uint32_t qcap, uint32_t scap, uint32_t sblk);
+// short-region (SH) kernels: SUM_I64, signal strategy, fused aggregate, K >= 1
+// stages, with their own ring / stage / signal-queue geometry (rs_k20s.cu);
+// main == nullptr where not built
+Launch short_launch_agg20(int K, uint32_t qcap, uint32_t scap, uint32_t sblk);
 // SUM_I64 + stage-1 drop counts delivered by a node-generated signal (rs_k27.cu)
 Launch launch_agg27(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
 

@@ -228,34 +228,37 @@ __device__ __noinline__ uint32_t partial_stage_ip(const Op op, uint32_t *ring, u
 // shared addresses: one LDS with an immediate offset per slice and an
 // LEA-formed store address (66 -> ~44 SASS per ensemble); an ensemble that
 // straddles the ring end takes the masked loop.
-template <class Op>
-__device__ __forceinline__ uint32_t filter_linear_ens(uint32_t si, uint32_t so, const Op &op, uint32_t lt) {
-    const uint32_t lane4 = (threadIdx.x & 31u) * 4u;
-    uint32_t v[IPL];
+template <int NS, class Op>
+__device__ __forceinline__ void filter_linear_ens(uint32_t si, uint32_t &so, const Op &op, uint32_t lt) {
+    // si: this lane's slot-0 load address; so: the output tail (byte address).
+    // NS slices (NS/4 ensembles): ensemble k's stores land below ensemble
+    // k+1's input slots (stable compaction never outruns the reads), so all
+    // loads may come first.
+    uint32_t v[NS];
 #pragma unroll
-    for (int j = 0; j < IPL; ++j) v[j] = lds32(si + lane4 + 128u * j);
+    for (int j = 0; j < NS; ++j) v[j] = lds32(si + 128u * j);
     __syncwarp();      // every lane's reads before any compaction store
-    bool keep[IPL];
-    uint32_t mk[IPL], c[IPL];
+    bool keep[NS];
+    uint32_t mk[NS];
 #pragma unroll
-    for (int j = 0; j < IPL; ++j) {
+    for (int j = 0; j < NS; ++j) {
         keep[j] = op(v[j]);
         mk[j] = __ballot_sync(kFull, keep[j]);
-        c[j] = __popc(mk[j]);
     }
-    uint32_t rel = 0;
+    // byte addresses kept out of the compiler's reassociation (it would
+    // rebuild them from a running count: one more add per slice)
 #pragma unroll
-    for (int j = 0; j < IPL; ++j) {
-        if (keep[j]) sts32(so + (rel + __popc(mk[j] & lt)) * 4u, v[j]);
-        rel += c[j];
+    for (int j = 0; j < NS; ++j) {
+        if (keep[j]) sts32(lea4(__popc(mk[j] & lt), so), v[j]);
+        so = lea4(__popc(mk[j]), so);
     }
-    return rel;
 }
 template <class Op>
 __device__ __noinline__ uint32_t filter_batch_ip(uint32_t *ring, uint32_t mask, uint32_t h, uint32_t nens, uint32_t tl,
                                                  const Op op) {
     const uint32_t lt = lanemask_lt();
     const uint32_t rb = smem_addr(ring);
+    const uint32_t lane4 = (threadIdx.x & 31u) * 4u;
     while (nens > 0) {
         const uint32_t hi = h & mask, ti = tl & mask;
         const uint32_t nl = min(nens, min((mask + 1 - hi) / W, (mask + 1 - ti) / W));
@@ -265,16 +268,12 @@ __device__ __noinline__ uint32_t filter_batch_ip(uint32_t *ring, uint32_t mask, 
             --nens;
             continue;
         }
-        uint32_t si = rb + hi * 4u, so = rb + ti * 4u, n = 0;
+        const uint32_t so0 = rb + ti * 4u;
+        uint32_t si = rb + hi * 4u + lane4, so = so0;
 #pragma unroll 1
-        for (uint32_t k = 0; k < nl; ++k) {
-            const uint32_t c = filter_linear_ens(si, so, op, lt);
-            si += 4u * W;
-            so += 4u * c;
-            n += c;
-        }
+        for (uint32_t k = 0; k < nl; ++k, si += 4u * W) filter_linear_ens<IPL>(si, so, op, lt);
         h += nl * W;
-        tl += n;
+        tl += (so - so0) >> 2;
         nens -= nl;
     }
     __syncwarp();
@@ -346,6 +345,14 @@ __device__ __noinline__ FusedAcc<AT> fused_batch(const uint32_t *in, uint32_t im
     return st;
 }
 
+// Fused node K, in-place ring, cheap lifts (the signal strategy's fused
+// aggregate over 4-byte items): ensembles that do not straddle the ring end
+// load with one immediate-offset LDS per slice; the straddling one goes
+// through the compact per-slice loop (fused_partial with e = w).
+template <class AT, class Op>
+__device__ __noinline__ FusedAcc<AT> fused_batch_ip(const uint32_t *ring, uint32_t mask, uint32_t h, uint32_t nens,
+                                                    const Op op, FusedAcc<AT> st);
+
 // In-place rings: move n items (and tags) ending at position `end` up by
 // `shift` positions -- a memmove toward higher positions in blocks of <= w
 // items, highest block first (each block is read completely before it is
@@ -404,6 +411,40 @@ __device__ __noinline__ FusedAcc<AT> fused_partial(const uint32_t *in, uint32_t 
     return st;
 }
 
+template <class AT, class Op>
+__device__ __noinline__ FusedAcc<AT> fused_batch_ip(const uint32_t *ring, uint32_t mask, uint32_t h, uint32_t nens,
+                                                    const Op op, FusedAcc<AT> st) {
+    const uint32_t rb = smem_addr(ring) + (threadIdx.x & 31u) * 4u;
+    while (nens > 0) {
+        const uint32_t hi = h & mask;
+        const uint32_t nl = min(nens, (mask + 1 - hi) / W);
+        if (nl == 0) {
+            st = fused_partial<AT, Op, false>(ring, mask, h, W, op, 0, 0u, st);
+            h += W;
+            --nens;
+            continue;
+        }
+        uint32_t si = rb + hi * 4u;
+#pragma unroll 1
+        for (uint32_t k = 0; k < nl; ++k, si += 4u * W) {
+            uint32_t v[IPL];
+#pragma unroll
+            for (int j = 0; j < IPL; ++j) v[j] = lds32(si + 128u * j);
+            typename AT::A part = AT::id();
+#pragma unroll
+            for (int j = 0; j < IPL; ++j) {
+                const bool keep = op(v[j]);
+                st.kept += keep ? 1u : 0u;
+                if (keep) part = AT::comb(part, AT::lift_i(v[j], 0));
+            }
+            st.acc = AT::comb(st.acc, part);
+        }
+        h += nl * W;
+        nens -= nl;
+    }
+    return st;
+}
+
 struct Chunk {
     int32_t k;             // chunk id (-1 = empty slot)
     long long beg, end;    // element range [beg, end)
@@ -444,7 +485,8 @@ static __device__ __noinline__ void load_pv(const uint32_t *ctx, const uint32_t 
     __syncwarp();
 }
 
-template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false, int HYB = 0, bool SPL = false>
+template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false, int HYB = 0, bool SPL = false,
+          bool SH = false>
 struct Pipe {
     using AT = AggT<AGG>;
     using A = typename AT::A;
@@ -567,6 +609,7 @@ struct Pipe {
     long long adelta;  // text aggregate: index offset of the current part (see part_delta)
     uint32_t dkey;     // tagged text aggregate: key whose delta is cached in adelta (per lane)
     uint32_t fkept;    // fused aggregate: items that reached it (per lane; node statistics)
+    bool adirty = false;   // SH: the generic data phase folded into acc since the last Begin/End
     uint32_t ekey = 0; // EMIT, signal strategy: key of the open region
     uint32_t ckey = 0; // hybrid converter node: key of the open region
     // RS_OP_SUM_I64_DROPS: stage 1 counts the items it drops per region part and
@@ -1131,7 +1174,9 @@ struct Pipe {
             }
             return;
         }
-        const FusedAcc<AT> r = fused_batch<AT, Op, AGG_U8IN>(in, imask, h, nens, op, adelta, P.C - 1, FusedAcc<AT>{acc, fkept});
+        FusedAcc<AT> r;
+        if constexpr (INPLACE && !AT::heavy) r = fused_batch_ip<AT, Op>(in, imask, h, nens, op, FusedAcc<AT>{acc, fkept});
+        else r = fused_batch<AT, Op, AGG_U8IN>(in, imask, h, nens, op, adelta, P.C - 1, FusedAcc<AT>{acc, fkept});
         acc = r.acc;
         fkept = r.kept;
     }
@@ -1224,6 +1269,134 @@ struct Pipe {
         }
     }
 
+    // ------------------------------------------ short-region batches (SH)
+    // Regions shorter than an ensemble (the left of the paper's sweep,
+    // P:568-589) make the signal strategy fire one partial ensemble and two
+    // signals per region at every node.  SH kernels keep that firing sequence
+    // (every ensemble bounded by its signal's credit; each signal
+    // consumed after exactly the items before it, Lemma 1) but run
+    // the per-signal bookkeeping warp-parallel: lane j holds pending signal j
+    // of the input edge (one warp load), the segment before it (the items its
+    // credit counts) is fired as one partial ensemble, and the forwarded
+    // signals are written with one warp store, lane j's credit being the
+    // survivors of segment j (sender rule 2; rule 1 for the first
+    // when the output signal queue was empty).  The fused aggregate
+    // folds each ensemble with two warp reductions (SUM_I64: 16-bit halves of
+    // the lane sums, exact) and stores the region's total at its End.
+    template <int n>
+    __device__ __forceinline__ bool try_short(uint32_t avail) {
+        if (P.st[n - 1].op == RS_OP_PARENT_LT) return false;   // per-region context: the general pass
+        bool r = false;
+        with_op_k(P.st[n - 1], 0u, [&](auto op) { r = short_batch<n>(op, avail); });
+        return r;
+    }
+    template <int n, class Op>
+    __device__ __forceinline__ bool short_batch(const Op op, uint32_t avail) {
+        constexpr int ei = n - 1;
+        constexpr bool AGGN = NA && n == K;
+        // cheap test first: the head segment must be shorter than an ensemble and
+        // all present (otherwise the general pass runs: full ensembles, or wait)
+        {
+            const uint32_t c0 = E<ei>().xfer ? E<ei>().cur : (S<ei>()[E<ei>().sh & smask].y & CREDIT_MASK);
+            if (c0 >= (uint32_t)W || c0 > avail) return false;
+        }
+        const uint32_t np = E<ei>().st - E<ei>().sh;
+        uint2 sg = make_uint2(0u, 0u);
+        if ((uint32_t)lane < np) sg = S<ei>()[(E<ei>().sh + lane) & smask];
+        // segment j = the items signal j's credit counts: the rest of a
+        // transferred head credit, else the signal's own credit
+        uint32_t e = sg.y & CREDIT_MASK;
+        if (lane == 0 && E<ei>().xfer) e = E<ei>().cur;
+        uint32_t cum = e;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(kFull, cum, d);
+            if (lane >= d) cum += o;
+        }
+        bool ok = (uint32_t)lane < np && e < (uint32_t)W && cum <= avail;
+        if constexpr (!AGGN) ok = ok && (uint32_t)lane < scap - (E<n>().st - E<n>().sh);   // forwarded signals fit
+        const uint32_t bad = ~__ballot_sync(kFull, ok);
+        const uint32_t k = bad ? (uint32_t)__ffs(bad) - 1u : 32u;   // leading run of batchable signals
+        if (k == 0) return false;
+        uint32_t *ring = Q<0>();
+        const uint32_t m = ring0 - 1;
+        const uint32_t h0 = E<ei>().qh;
+        const uint32_t excl = cum - e;                 // lane j: segment j starts at h0 + excl
+        // the non-empty segments, in stream order (back-to-back signals have none)
+        uint32_t nz = __ballot_sync(kFull, e != 0) & (k == 32u ? 0xffffffffu : ((1u << k) - 1u));
+        const uint32_t nparts = __popc(nz);
+        if constexpr (!AGGN) {
+            const uint32_t tl_in = E<n>().qt;
+            uint32_t tl = tl_in, sj = 0;
+            while (nz) {
+                const uint32_t j = __ffs(nz) - 1;
+                nz &= nz - 1u;
+                const uint32_t ej = __shfl_sync(kFull, e, j);
+                const uint32_t h = h0 + __shfl_sync(kFull, excl, j);
+                uint32_t t2;
+                if (ej <= 32u) {               // one slice, inline
+                    const bool act = (uint32_t)lane < ej;
+                    uint32_t v = act ? ring[(h + lane) & m] : 0u;
+                    __syncwarp();              // every lane's reads before the stores
+                    const bool keep = act && op(v);
+                    const uint32_t mk = __ballot_sync(kFull, keep);
+                    if (keep) ring[(tl + __popc(mk & lt)) & m] = v;
+                    t2 = tl + __popc(mk);
+                } else {
+                    t2 = partial_stage_ip(op, ring, m, h, ej, tl);
+                }
+                if ((uint32_t)lane == j) sj = t2 - tl;
+                tl = t2;
+            }
+            __syncwarp();
+            uint32_t c = sj;                   // rule 2: survivors since the previous signal
+            if (lane == 0) c = (E<n>().sh == E<n>().st) ? (tl_in + sj - E<n>().qh) : (E<n>().sent + sj);
+            if ((uint32_t)lane < k) S<n>()[(E<n>().st + lane) & smask] = make_uint2(sg.x, c | (sg.y & END_BIT));
+            E<n>().st += k;
+            E<n>().sent = 0;
+            E<n>().qt = tl;
+        } else {
+            static_assert(!SH || AGG == 20, "short-region batches are built for SUM_I64");
+            // lane j: the fold of segment j (its region's items in this batch)
+            A rv = AT::id();
+            if (adirty) {                      // the head End closes a region the general pass began folding
+                const A t = warp_reduce<AT>(acc);
+                if (lane == 0) rv = t;
+                acc = AT::id();
+                adirty = false;
+            }
+            while (nz) {
+                const uint32_t j = __ffs(nz) - 1;
+                nz &= nz - 1u;
+                const uint32_t ej = __shfl_sync(kFull, e, j);
+                const uint32_t h = h0 + __shfl_sync(kFull, excl, j);
+                long long ls = 0;
+                for (uint32_t o = 0; o < ej; o += 32u) {
+                    const uint32_t idx = o + lane;
+                    uint32_t x = idx < ej ? ring[(h + idx) & m] : 0u;
+                    if (idx < ej && op(x)) {
+                        ls += (int)x;
+                        ++fkept;
+                    }
+                }
+                // exact: each lane sum = (ls >> 16) * 2^16 + (ls & 0xffff), both halves small
+                const int lo = __reduce_add_sync(kFull, (int)((uint32_t)ls & 0xffffu));
+                const int hi = __reduce_add_sync(kFull, (int)(ls >> 16));
+                if ((uint32_t)lane == j) rv += (A)((long long)hi * 65536ll + (long long)lo);
+            }
+            // a::end of every region closed in the batch: push(acc); Begin: identity
+            if ((uint32_t)lane < k && (sg.y & END_BIT)) store_key(sg.x, rv);
+        }
+        E<ei>().qh = h0 + __shfl_sync(kFull, cum, k - 1);
+        E<ei>().sh += k;
+        E<ei>().cur = 0;
+        E<ei>().xfer = false;
+        stat_add(n, 0, nparts);
+        stat_add(n, 1, __shfl_sync(kFull, cum, k - 1));
+        __syncwarp();
+        return true;
+    }
+
     // Fire node n (1..K+1) repeatedly while it can make progress: data phase,
     // then signal phase, full-first (A8).
     template <int n>
@@ -1237,6 +1410,23 @@ struct Pipe {
         uint32_t ready_lim = 0;
         if (ei == 0) ready_lim = landed_pos();
         for (;;) {
+            if constexpr (SH && !TGE<ei>) {
+                // short regions: a warp-parallel batch of signals and the partial
+                // ensembles they bound (short_batch); the general pass below runs
+                // whenever the head segment is an ensemble or longer
+                if (E<ei>().sh != E<ei>().st) {
+                    uint32_t av = E<ei>().qt - E<ei>().qh;
+                    if (ei == 0) {
+                        if ((int)(ready_lim - E<0>().qh) < (int)av) ready_lim = landed_pos();
+                        const int rdy = (int)(ready_lim - E<0>().qh);
+                        av = rdy <= 0 ? 0u : min(av, (uint32_t)rdy);
+                    }
+                    if (try_short<n>(av)) {
+                        prog = true;
+                        continue;
+                    }
+                }
+            }
             bool spend;
             const uint32_t a = admissible<ei>(spend);
             uint32_t ar = a;
@@ -1256,6 +1446,7 @@ struct Pipe {
                 const uint32_t nens = lim / W;
                 if constexpr (TR) if (P.trace) trace_ens(n, in, imask, E<ei>().qh, nens * W);
                 run_full<n>(in, tin, imask, E<ei>().qh, nens);
+                if constexpr (SH && AGGN) adirty = true;
                 E<ei>().qh += nens * W;
                 if (spend) E<ei>().cur -= nens * W;
                 lim -= nens * W;
@@ -1269,6 +1460,7 @@ struct Pipe {
                 if (bounded || dr) {
                     if constexpr (TR) if (P.trace) trace_ens(n, in, imask, E<ei>().qh, lim);
                     run_partial<n>(in, tin, imask, E<ei>().qh, lim);
+                    if constexpr (SH && AGGN) adirty = true;
                     E<ei>().qh += lim;
                     if (spend) E<ei>().cur -= lim;
                     stat_add(n, 0, 1u);            // partial ensembles and their items; full
@@ -1334,6 +1526,7 @@ struct Pipe {
                         if (lane == 0) store_key(hs.x, v);
                         acc = AT::id();
                     }
+                    if constexpr (SH) adirty = false;
                 } else if constexpr (TGE<n>) {
                     if (!is_end) ckey = hs.x;    // hybrid converter: outputs carry this key as their tag
                 } else {
@@ -1527,6 +1720,23 @@ struct Pipe {
         uint32_t ready_lim = 0;
         if (ei == 0) ready_lim = landed_pos();
         for (;;) {
+            if constexpr (SH && !TGE<ei>) {
+                // short regions: a warp-parallel batch of signals and the partial
+                // ensembles they bound (short_batch); the general pass below runs
+                // whenever the head segment is an ensemble or longer
+                if (E<ei>().sh != E<ei>().st) {
+                    uint32_t av = E<ei>().qt - E<ei>().qh;
+                    if (ei == 0) {
+                        if ((int)(ready_lim - E<0>().qh) < (int)av) ready_lim = landed_pos();
+                        const int rdy = (int)(ready_lim - E<0>().qh);
+                        av = rdy <= 0 ? 0u : min(av, (uint32_t)rdy);
+                    }
+                    if (try_short<n>(av)) {
+                        prog = true;
+                        continue;
+                    }
+                }
+            }
             bool spend;
             const uint32_t a = admissible<ei>(spend);
             uint32_t ar = a;
@@ -2224,15 +2434,17 @@ struct Pipe {
     }
 };
 
-template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false, int HYB = 0, bool SPL = false>
+template <int K, int AGG, bool TAG, bool FUSE, bool CTX = false, bool TR = false, int HYB = 0, bool SPL = false,
+          bool SH = false>
 __global__ void __launch_bounds__(WPB_MAX * 32, 1) k_pipeline(const __grid_constant__ KParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    using PP = Pipe<K, AGG, TAG, FUSE, CTX, TR, HYB, SPL>;
+    using PP = Pipe<K, AGG, TAG, FUSE, CTX, TR, HYB, SPL, SH>;
     uint8_t *mine = smem + (size_t)warp * PP::smem_bytes(P.qcap, P.scap, P.ring0);
     if (P.hdr->err) return;
     if (P.auto_sel && P.hdr->sel != P.auto_sel - 1) return;   // AUTO: the other strategy's kernel runs
+    if (P.short_sel && P.hdr->ssel != P.short_sel - 1) return; // the other (short / long region) kernel runs
     PP pipe(P, mine, lane);
     pipe.run();
 }
