@@ -1,7 +1,7 @@
 """Small cases of every strategy / mode / exit for compute-sanitizer (GPU box):
 signal, tagged, context, hybrid, AUTO; fused and unfused; the element-wise
 exit and the taxi parser; parent contexts; the trace kernels; the text SWAR
-path.  Prints mismatches against the oracle (expected: none)."""
+path; the short-region kernel.  Prints mismatches against the oracle (expected: none)."""
 import os
 import sys
 
@@ -46,6 +46,17 @@ for L in (3, 100):
                 bad += nb
                 if nb or code:
                     print("MISMATCH", L, K, strat, fl, nb, code)
+    # short-region kernel (RS_FLAG_SHORT_ON), default and small geometry
+    for K in (1, 3):
+        st = synth.sweep_stages(K)
+        ref = oracle.brute(vals, off, st, "sum_i64")[0]
+        for kw in ({}, {"queue_cap": 512, "signal_cap": 4, "q0_stage": 128}):
+            p = rs.Pipeline(st, "sum_i64", flags=rs.RS_FLAG_STATS | rs.RS_FLAG_SHORT_ON, grid=2, chunk=2048, **kw)
+            got, code = run(p, vals, off)
+            nb = int((got[0] != ref).sum())
+            bad += nb + (code != 0)
+            if nb or code:
+                print("SHORT MISMATCH", L, K, kw, nb, code)
     # parent context, trace kernels
     ctx = np.random.default_rng(L).integers(0, 2**32, off.size - 1, dtype=np.uint64).astype(np.uint32)
     st = [("hash_lt", 0x9E3779B1, 192), ("parent_lt", ctx)]
