@@ -730,6 +730,12 @@ def run_sweep(rs, torch, dev, args):
                 e.update({"dist": dist_, "L": L, "sawtooth": L not in Ls})
                 if strat == "signal":
                     e["bound"] = bound
+                    # the prepass's rule (rs.h RS_FLAG_SHORT_ON): short-region kernel below 96 children/region
+                    e["kernel"] = "short-region" if e["children"] < 96 * e["regions"] else "general"
+                res.append(e)
+            if L in Ls and L < 96:             # the general signal kernel at the same point
+                e = _time_point(rs, torch, dev, args, vals, off, stages3, "sum_i64", "signal", rs.RS_FLAG_SHORT_OFF)
+                e.update({"dist": dist_, "L": L, "sawtooth": False, "kernel": "general", "bound": bound})
                 res.append(e)
             if L in (256, 4096):
                 e = _time_point(rs, torch, dev, args, vals, off, stages3, "sum_i64", "signal", rs.RS_FLAG_UNFUSED)

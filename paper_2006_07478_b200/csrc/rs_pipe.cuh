@@ -1069,7 +1069,7 @@ struct Pipe {
             cb = base0 + (long long)k * P.C;
         } else {
             r = key;
-            const long long k = (P.off[r] - base0) / P.C;
+            const long long k = (P.off[r] - base0) >> (__ffs(P.C) - 1);   // C is a power of 2; off[r] >= base0
             cb = base0 + k * P.C;
         }
         return cb - P.off[r];
@@ -1136,6 +1136,42 @@ struct Pipe {
         }
     }
 
+    // NG (4 or 8) full ensembles of the text stream at once (NG x 128 bytes,
+    // still NG firings of the fused node inside one region): lane l tests its
+    // word of each (match4), the survivor masks are packed into one mask
+    // (bit 4j + b = byte b of ensemble j), and the survivors of all NG are
+    // lifted in one divergent walk -- far fewer iterations than NG separate
+    // walks.  Every survivor is the class byte c itself
+    // (single-member class), so only its position is needed; the count half
+    // of the aggregate adds the popcount once.
+    template <int NG>
+    __device__ __forceinline__ void swar_group(const uint32_t *in, uint32_t imask, uint32_t h, const OpClass1 &op) {
+        const uint32_t wmask = imask >> 2;
+        const uint32_t a = h & 3u;
+        const uint32_t wi = (h >> 2) + lane;
+        uint32_t pk = 0;
+#pragma unroll
+        for (int j = 0; j < NG; ++j) {
+            uint32_t w = in[(wi + 32u * j) & wmask];
+            if (a) w = __funnelshift_r(w, in[(wi + 32u * j + 1u) & wmask], 8u * a);
+            // 0x80 per matching byte -> one bit per byte (bits 0..3) -> nibble j
+            const uint32_t m = (op.match4(w) >> 7) * 0x00204081u;   // bytes' bits gathered in bits 21..24
+            pk |= ((m >> 21) & 0xfu) << (4 * j);
+        }
+        const uint32_t nk = __popc(pk);
+        fkept += nk;
+        acc.x += nk;
+        const uint32_t cm = P.C - 1, c = op.c4 & 0xffu;
+        while (__any_sync(kFull, pk != 0)) {
+            if (pk) {
+                const uint32_t bit = __ffs(pk) - 1;
+                pk &= pk - 1u;
+                const uint32_t pos = h + ((bit >> 2) << 7) + 4u * lane + (bit & 3u);
+                acc.y ^= AT::lift_i(c | ((pos & cm) << 8), adelta).y;
+            }
+        }
+    }
+
     // Fused node K, full ensembles (signal strategy): apply the op, fold the
     // survivors into the per-lane accumulator (isGood + a::run).
     template <class Op>
@@ -1145,7 +1181,10 @@ struct Pipe {
             return;
         }
         if constexpr (K == 1 && AGG_U8IN && AT::heavy && std::is_same<Op, OpClass1>::value) {
-            for (uint32_t k = 0; k < nens; ++k, h += W) swar_ens(in, imask, h, W, op);
+            uint32_t k = 0;
+            for (; k + 8 <= nens; k += 8, h += 8 * W) swar_group<8>(in, imask, h, op);
+            for (; k + 4 <= nens; k += 4, h += 4 * W) swar_group<4>(in, imask, h, op);
+            for (; k < nens; ++k, h += W) swar_ens(in, imask, h, W, op);
             return;
         }
         if constexpr (K == 1) {
