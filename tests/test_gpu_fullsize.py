@@ -7,6 +7,8 @@ Configs (bench.workload_spec, DESIGN.md §8 input recipe):
   Zipf(1.2) region lengths, N = 2^30 int32            (configs[4], 1-GPU point)
   R-MAT scale 24 CSR, 2^28 u32 edge weights           (configs[2])
   4 GiB text, lines as regions (offsets reach 2^32)   (configs[3])
+  sweep fixed L = 1 and U{0..8} (L = 4), N = 2^29     (configs[1], short end: the
+                                                       short-region signal kernel)
 each under the signal, tagged, per-lane context (4-byte elements) and AUTO
 strategies.  Integer aggregates are compared bit-exactly.
 """
@@ -40,7 +42,8 @@ def _host(t):
     return x
 
 
-@pytest.mark.parametrize("workload", ["sweep_fixed_L4096", "sweep_var_L4096", "zipf", "graph", "text"])
+@pytest.mark.parametrize("workload", ["sweep_fixed_L4096", "sweep_var_L4096", "zipf", "graph", "text",
+                                      "sweep_fixed_L1", "sweep_var_L4"])
 def test_full_size_all_regions(rs, workload):
     import bench
     spec = bench.workload_spec(workload)
@@ -58,8 +61,11 @@ def test_full_size_all_regions(rs, workload):
         assert int(oh[-1]) == 1 << 32          # the last line ends at byte 2^32: indices past u32
     ref = oracle.brute_sharded(vh, oh, spec["stages"], spec["agg"])
     strategies = ["signal", "tagged", "auto"] + (["context"] if spec["dtype"] != "u8" else [])
+    if spec["L"] and spec["L"] < 96:           # the short-region kernel (default choice) and the general one
+        strategies = [("signal", 0), ("signal", rs.RS_FLAG_SHORT_OFF), "tagged"]
     for strat in strategies:
-        p = rs.Pipeline(spec["stages"], spec["agg"], strategy=strat)
+        strat, fl = strat if isinstance(strat, tuple) else (strat, 0)
+        p = rs.Pipeline(spec["stages"], spec["agg"], strategy=strat, flags=rs.RS_FLAG_STATS | fl)
         out = p.alloc_outputs(R, dev)
         ws = p.alloc_workspace(R, vals.numel(), dev)
         p.run(vals, off, out, ws)
