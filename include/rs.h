@@ -181,7 +181,7 @@ typedef struct {
                                 sequential scheduler: all queues share ONE in-place ring of
                                 max(4*q0_stage, min(queue_cap, 8*q0_stage)) items, raised to fit one
                                 partial ensemble per queue plus a stage (0 = auto: 32w signal, 16w
-                                tagged).  u8 elements: capacity of each inter-stage queue
+                                tagged, 8w tagged with 0-1 stages).  u8 elements: capacity of each inter-stage queue
                                 (0 = auto: 8w with 2+ stages, else 16w). */
     uint32_t signal_cap;     /* signal queue capacity (entries, power of 2, >= 4; 0 = auto) */
     int32_t grid;            /* persistent CTAs; 0 = fill the device                  */
@@ -189,8 +189,8 @@ typedef struct {
     uint32_t flags;          /* RS_FLAG_*                                            */
     uint32_t q0_stage;       /* elements per TMA stage of the enumerate queue (the ring holds 4..8
                                 stages); power of 2 in [128, 4096], <= chunk; 0 = auto (in-place
-                                rings: 1024 signal, 512 tagged; otherwise 256 tagged or 2+ stages,
-                                else 512) */
+                                rings: 1024 signal, 512 tagged, 256 tagged with 0-1 stages;
+                                otherwise 256 tagged or 2+ stages, else 2048) */
     uint32_t auto_min_len;   /* RS_STRATEGY_AUTO: mean children per region at and above which the
                                 signal strategy runs; 0 = the crossover measured on B200 for the
                                 pipeline's stage count */

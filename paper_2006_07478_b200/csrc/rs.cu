@@ -334,11 +334,15 @@ rs_status rs_pipeline_create(const rs_node *nodes, int n_nodes, rs_dtype elem, c
     // (profiles/r1_tuning.txt).
     const bool inplace = elem != RS_U8;
     const bool tagged_ = cfg.strategy == RS_STRATEGY_TAGGED || cfg.strategy == RS_STRATEGY_HYBRID;
-    if (cfg.queue_cap == 0) cfg.queue_cap = inplace ? (tagged_ ? 16 * W : 32 * W) : (nst_ >= 2 ? 8 * W : 16 * W);
+    // (tagged with 0-1 stages, e.g. the R-MAT graph: an 8w ring in stages of 2w fits
+    // 20 instances per SM: 1.41 -> 1.17 ms, profiles/r2_tuning.txt)
+    if (cfg.queue_cap == 0)
+        cfg.queue_cap = inplace ? (tagged_ ? (nst_ <= 1 ? 8 * W : 16 * W) : 32 * W) : (nst_ >= 2 ? 8 * W : 16 * W);
     if (cfg.signal_cap == 0)
         cfg.signal_cap = inplace ? 32 : (nst_ >= 2 ? 64 : 128);   // (context strategy: profiles/r1_tuning.txt)
     if (cfg.q0_stage == 0)
-        cfg.q0_stage = inplace ? (tagged_ ? 512 : 1024) : ((tagged_ || nst_ >= 2) ? 256 : 2048);   // byte streams: SWAR wants big stages
+        cfg.q0_stage = inplace ? (tagged_ ? (nst_ <= 1 ? 256 : 512) : 1024)
+                               : ((tagged_ || nst_ >= 2) ? 256 : 2048);   // byte streams: SWAR wants big stages
     if (!is_pow2(cfg.queue_cap) || cfg.queue_cap < 2 * W || cfg.queue_cap > 65536)
         return fail(RS_ERR_UNSUPPORTED, "queue_cap must be a power of 2 in [256, 65536]");
     if (!is_pow2(cfg.signal_cap) || cfg.signal_cap < 4 || cfg.signal_cap > 65536)
