@@ -1512,9 +1512,12 @@ struct Pipe {
             // signal with a positive credit moves it into the counter (rule 2b)
             // so the next data phase starts without re-reading the queue.
             if (TGE<ei> || !spend || E<ei>().cur != 0) {
-                if (!did) break;
-                prog = true;
-                continue;
+                // no signal to consume: the data phase took everything admissible
+                // (what is left is < w items, or waits for its credit) and nothing
+                // upstream runs meanwhile -- another pass could only find newly
+                // landed TMA stages, which the next sweep picks up
+                prog |= did;
+                break;
             }
             uint32_t nsig = 0;
             for (;;) {
