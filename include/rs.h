@@ -299,10 +299,12 @@ rs_status rs_pipeline_check(rs_pipeline *p, rs_stream stream, int32_t *code);
  * `stream`): ms[0] = prepass, ms[1] = persistent pipeline kernel, ms[2] = fixup. */
 rs_status rs_pipeline_kernel_times(rs_pipeline *p, float *ms3, rs_stream stream);
 
-/* Number of kernel launches the last rs_pipeline_run enqueued. */
+/* Number of kernel launches the last rs_pipeline_run enqueued (4 when AUTO or the short-region
+ * choice enqueued two main kernels, one of which exits at once). */
 int rs_pipeline_launches(const rs_pipeline *p);
 
-/* Persistent CTAs and warps (pipeline instances) per CTA of the last run. */
+/* Persistent CTAs and warps (pipeline instances) per CTA of the last run's general kernel (the
+ * short-region kernel, RS_FLAG_SHORT_ON, sizes its own launch from its own geometry). */
 rs_status rs_pipeline_geometry(const rs_pipeline *p, int32_t *grid, int32_t *warps_per_cta,
                                int32_t *chunk);
 
