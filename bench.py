@@ -766,7 +766,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="sweep_fixed_L4096")
-    ap.add_argument("--strategy", default="signal", choices=["signal", "tagged", "context", "auto"])
+    ap.add_argument("--strategy", default=None, choices=["signal", "tagged", "context", "auto"],
+                    help="default: signal for the sweep workloads (the headline), auto for zipf / graph / text")
     ap.add_argument("--no-sweep", dest="sweep", action="store_false")
     ap.add_argument("--sweep-L", default="1,4,32,256,4096")
     ap.add_argument("--sweep-reps", type=int, default=2)
@@ -777,6 +778,8 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--gather", default="peer", choices=["peer", "nccl"])
     args = ap.parse_args()
+    if args.strategy is None:
+        args.strategy = "signal" if args.workload.startswith("sweep") else "auto"
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
