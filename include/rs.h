@@ -152,7 +152,7 @@ enum {
                                 bracketing, unmixed ensembles and per-bracket counts.  A
                                 separate kernel instantiation: no cost when off. */
     RS_FLAG_SHORT_OFF = 128u,/* never use the short-region kernel (see RS_FLAG_SHORT_ON)  */
-    RS_FLAG_SHORT_ON = 256u, /* signal strategy, SUM_I64, fused aggregate, 1+ stages: always run
+    RS_FLAG_SHORT_ON = 256u, /* signal strategy, SUM_I64 or COUNT_MIN_U32, fused aggregate, 1+ stages: always run
                                 the short-region kernel.  It fires the same ensembles and
                                 consumes the same signals in the same order as the general
                                 kernel (identical results and counters) but handles up to 32

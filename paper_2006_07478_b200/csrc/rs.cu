@@ -572,13 +572,14 @@ static rs_status run_impl(rs_pipeline *p, const void *d_elems, int64_t n_elems, 
     // 16 instances per SM (profiles/r2_tuning.txt)
     Launch shl{};
     Prep ps = pa;
-    if (!is_auto && p->agg == RS_OP_SUM_I64 && p->cfg.strategy == RS_STRATEGY_SIGNAL && p->nst >= 1 &&
+    if (!is_auto && (p->agg == RS_OP_SUM_I64 || p->agg == RS_OP_COUNT_MIN_U32) && p->cfg.strategy == RS_STRATEGY_SIGNAL &&
+        p->nst >= 1 &&
         !(p->cfg.flags & (RS_FLAG_UNFUSED | RS_FLAG_TRACE | RS_FLAG_PROFILE | RS_FLAG_SHORT_OFF)) &&
         ((p->cfg.flags & RS_FLAG_SHORT_ON) || n_elems < 2ll * W * n_regions)) {
         const uint32_t qc = p->geom_default ? 16 * W : p->cfg.queue_cap;
         const uint32_t sc = p->geom_default ? 128 : p->cfg.signal_cap;
         const uint32_t sb = p->geom_default ? 4 * W : p->cfg.q0_stage;
-        shl = short_launch_agg20(p->nst, qc, sc, sb);
+        shl = p->agg == RS_OP_SUM_I64 ? short_launch_agg20(p->nst, qc, sc, sb) : short_launch_agg22(p->nst, qc, sc, sb);
         if (shl.main) {
             if (!ensure_smem_attr(shl.main, p->device)) return fail(RS_ERR_CUDA, "cannot raise the kernel's shared-memory limit");
             if (p->sh_grid == 0) {

@@ -242,10 +242,11 @@ Launch launch_agg20_hybrid(int K, bool fuse, int hyb, uint32_t qcap, uint32_t sc
 Launch launch_agg25_hybrid(int K, bool fuse, int hyb, uint32_t qcap, uint32_t scap, uint32_t sblk);
 // fan-out (SPLIT + two leaf SUM_I64 aggregates; rs_k26.cu), K <= 2 stages before the split
 Launch launch_agg26_split(int K, uint32_t qcap, uint32_t scap, uint32_t sblk);
-// short-region (SH) kernels: SUM_I64, signal strategy, fused aggregate, K >= 1
+// short-region (SH) kernels: SUM_I64 / COUNT_MIN_U32, signal strategy, fused aggregate, K >= 1
 // stages, with their own ring / stage / signal-queue geometry (rs_k20s.cu);
 // main == nullptr where not built
 Launch short_launch_agg20(int K, uint32_t qcap, uint32_t scap, uint32_t sblk);
+Launch short_launch_agg22(int K, uint32_t qcap, uint32_t scap, uint32_t sblk);   // COUNT_MIN_U32 (rs_k22s.cu)
 // SUM_I64 + stage-1 drop counts delivered by a node-generated signal (rs_k27.cu)
 Launch launch_agg27(int K, bool tag, bool fuse, uint32_t qcap, uint32_t scap, uint32_t sblk, bool ctx);
 

@@ -1329,6 +1329,39 @@ struct Pipe {
         with_op_k(P.st[n - 1], 0u, [&](auto op) { r = short_batch<n>(op, avail); });
         return r;
     }
+    // One segment (< w items at h) through the fused node's op, folded and
+    // reduced over the warp with REDUX: SUM_I64 from the 16-bit halves of the
+    // lane sums (exact), COUNT_MIN_U32 as a sum and a min.
+    template <class Op>
+    __device__ __forceinline__ A seg_fold(const uint32_t *ring, uint32_t m, uint32_t h, uint32_t ej, const Op &op) {
+        if constexpr (AGG == 20) {
+            long long ls = 0;
+            for (uint32_t o = 0; o < ej; o += 32u) {
+                const uint32_t idx = o + lane;
+                uint32_t x = idx < ej ? ring[(h + idx) & m] : 0u;
+                if (idx < ej && op(x)) {
+                    ls += (int)x;
+                    ++fkept;
+                }
+            }
+            // each lane sum = (ls >> 16) * 2^16 + (ls & 0xffff), both halves small
+            const int lo = __reduce_add_sync(kFull, (int)((uint32_t)ls & 0xffffu));
+            const int hi = __reduce_add_sync(kFull, (int)(ls >> 16));
+            return (A)((long long)hi * 65536ll + (long long)lo);
+        } else {
+            uint32_t c = 0, mn = 0xffffffffu;
+            for (uint32_t o = 0; o < ej; o += 32u) {
+                const uint32_t idx = o + lane;
+                uint32_t x = idx < ej ? ring[(h + idx) & m] : 0u;
+                if (idx < ej && op(x)) {
+                    ++c;
+                    mn = min(mn, x);
+                }
+            }
+            fkept += c;
+            return make_uint2(__reduce_add_sync(kFull, c), __reduce_min_sync(kFull, mn));
+        }
+    }
     template <int n, class Op>
     __device__ __forceinline__ bool short_batch(const Op op, uint32_t avail) {
         constexpr int ei = n - 1;
@@ -1395,7 +1428,7 @@ struct Pipe {
             E<n>().sent = 0;
             E<n>().qt = tl;
         } else {
-            static_assert(!SH || AGG == 20, "short-region batches are built for SUM_I64");
+            static_assert(!SH || AGG == 20 || AGG == 22, "short-region batches are built for SUM_I64, COUNT_MIN_U32");
             // lane j: the fold of segment j (its region's items in this batch)
             A rv = AT::id();
             if (adirty) {                      // the head End closes a region the general pass began folding
@@ -1409,19 +1442,8 @@ struct Pipe {
                 nz &= nz - 1u;
                 const uint32_t ej = __shfl_sync(kFull, e, j);
                 const uint32_t h = h0 + __shfl_sync(kFull, excl, j);
-                long long ls = 0;
-                for (uint32_t o = 0; o < ej; o += 32u) {
-                    const uint32_t idx = o + lane;
-                    uint32_t x = idx < ej ? ring[(h + idx) & m] : 0u;
-                    if (idx < ej && op(x)) {
-                        ls += (int)x;
-                        ++fkept;
-                    }
-                }
-                // exact: each lane sum = (ls >> 16) * 2^16 + (ls & 0xffff), both halves small
-                const int lo = __reduce_add_sync(kFull, (int)((uint32_t)ls & 0xffffu));
-                const int hi = __reduce_add_sync(kFull, (int)(ls >> 16));
-                if ((uint32_t)lane == j) rv += (A)((long long)hi * 65536ll + (long long)lo);
+                const A t = seg_fold(ring, m, h, ej, op);
+                if ((uint32_t)lane == j) rv = AT::comb(rv, t);
             }
             // a::end of every region closed in the batch: push(acc); Begin: identity
             if ((uint32_t)lane < k && (sg.y & END_BIT)) store_key(sg.x, rv);

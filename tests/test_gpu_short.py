@@ -120,6 +120,34 @@ def test_short_parent_context(rs):
     _compare(rs, vals, off, stages, parent_ctx=ctx)
 
 
+@pytest.mark.parametrize("L", [1, 5, 40, 130])
+def test_short_count_min(rs, L):
+    """COUNT_MIN_U32 (the R-MAT config's aggregate): count and min per region
+    through the short-region kernel, against the oracle and the general
+    kernel's counters."""
+    lens = synth.lengths(15000 if L < 64 else 3000, "var", L=L, seed=L + 3)
+    off = synth.offsets(lens, base=1)
+    vals = synth.values(int(off[-1]) + 2, "u32", seed=L + 4)
+    for stages in ([("lt_u32", 1 << 31)], [("lt_u32", 3 << 30), ("lt_u32", 1 << 31)]):
+        ref = oracle.brute(vals, off, stages, "count_min_u32")
+        got = []
+        for fl in (rs.RS_FLAG_SHORT_ON, rs.RS_FLAG_SHORT_OFF):
+            p = rs.Pipeline(stages, "count_min_u32", strategy="signal", flags=rs.RS_FLAG_STATS | fl, chunk=2048)
+            e = torch.from_numpy(vals.view(np.int32)).cuda()
+            o = torch.from_numpy(off).cuda()
+            R = off.size - 1
+            out = p.alloc_outputs(R)
+            ws = p.alloc_workspace(R, e.numel())
+            p.run(e, o, out, ws)
+            torch.cuda.synchronize()
+            assert p.check() == 0
+            res = [t.cpu().numpy().view(np.uint32) for t in out]
+            for g, r in zip(res, ref):
+                np.testing.assert_array_equal(g, r)
+            got.append(np.array(p.stats()))
+        np.testing.assert_array_equal(got[0], got[1])
+
+
 def test_short_default_choice(rs):
     """Default flags: both kernels are enqueued for short-looking calls and the
     prepass picks by the call's own children count; either way the results
