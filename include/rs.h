@@ -185,7 +185,12 @@ typedef struct {
                                 (0 = auto: 8w with 2+ stages, else 16w). */
     uint32_t signal_cap;     /* signal queue capacity (entries, power of 2, >= 4; 0 = auto) */
     int32_t grid;            /* persistent CTAs; 0 = fill the device                  */
-    uint32_t chunk;          /* children per parent-stream claim; 0 = default        */
+    uint32_t chunk;          /* children per parent-stream claim (power of 2); 0 = auto: 32768 for
+                                4-byte signal / context pipelines, else 8192; with auto on those
+                                4-byte signal / context pipelines the part of the stream left after
+                                whole rounds of chunks
+                                over all instances is claimed in pieces of chunk/8 (no ragged last
+                                round; the prepass decides from the call's children) */
     uint32_t flags;          /* RS_FLAG_*                                            */
     uint32_t q0_stage;       /* elements per TMA stage of the enumerate queue (the ring holds 4..8
                                 stages); power of 2 in [128, 4096], <= chunk; 0 = auto (in-place

@@ -71,6 +71,7 @@ struct WsHdr {
     uint32_t nchunks;
     int32_t sel;         // strategy the run uses (0 signal, 1 tagged; RS_STRATEGY_AUTO decides on the device)
     int32_t ssel;        // signal strategy: 1 = the short-region (SH) kernel runs, 0 = the general one
+    uint32_t k1;         // chunks 0..k1-1 are C long, the later ones C >> TAIL_SH (see chunk_start)
     long long base0;     // align_down(offsets[0], 16 bytes)
     long long off0, offR;
 };
@@ -87,6 +88,8 @@ struct KParams {
     unsigned long long *stats;      // [(K+2) * 4]
     long long max_chunks;
     uint32_t C;                     // chunk length (children)
+    uint32_t tail;                  // 1: the last round of chunks is cut into C >> TAIL_SH pieces
+    uint32_t nwarps;                //    (whole rounds of C per instance first; see chunk_start)
     uint32_t qcap, scap;            // queue / signal capacities (powers of 2)
     uint32_t q0_stage;              // Q0 TMA stage size in elements (sequential kernel)
     uint32_t ring0;                 // Q0 ring capacity in elements (sequential kernel; in-place: all queues)
@@ -107,6 +110,18 @@ struct KParams {
     uint32_t *trace;                // RS_FLAG_TRACE: [0] events written, events of 8 words from word 8
     uint32_t trace_cap;             // events the buffer holds
 };
+
+// Chunk boundaries (the parent stream cut into claims).  Chunks
+// 0 .. k1-1 are C children long; the rest of the stream -- less than one round
+// of C per instance -- is cut into pieces of C >> TAIL_SH, so the last round
+// ends within a small piece's time on every instance instead of leaving the
+// instances that drew one chunk fewer idle for a whole chunk (with 8.5 chunks
+// per instance: 9 rounds -> 8 5/8).  Pieces stay powers of 2 (aligned with
+// power-of-2 regions).  Byte streams keep uniform chunks (k1 = all).
+constexpr int TAIL_SH = 3;
+__device__ __forceinline__ long long chunk_start(long long base0, long long k, long long C, long long k1) {
+    return k <= k1 ? base0 + k * C : base0 + k1 * C + ((k - k1) * C >> TAIL_SH);
+}
 
 // ------------------------------------------------------------ stage ops
 // isGood() / push() bodies (Fig. 5); readings A13/A14.
@@ -143,7 +158,19 @@ __global__ void k_prepass(KParams P) {
     const long long esz = P.esize;
     const long long base0 = (off0 * esz / align) * align / esz;
     long long span = offR - base0;
-    long long nch = span <= 0 ? 1 : (span + P.C - 1) / P.C;
+    const long long C = P.C;
+    long long nch = span <= 0 ? 1 : (span + C - 1) / C;
+    long long k1 = nch;
+    if (P.tail && span > 0) {
+        const long long nw = P.nwarps > 0 ? P.nwarps : 1;
+        const long long cs = C >> TAIL_SH;
+        const long long kk = (span / (C * nw)) * nw;                   // whole rounds of C
+        const long long n2 = kk + (span - kk * C + cs - 1) / cs;
+        if (n2 <= P.max_chunks) {
+            k1 = kk;
+            nch = n2;
+        }
+    }
     bool bad = nch > P.max_chunks || offR < off0 || off0 < 0 || offR > P.n_elems;
     if (bad) nch = 0;
     bool tagged = P.tagged > 0;
@@ -151,6 +178,7 @@ __global__ void k_prepass(KParams P) {
     if (tid == 0) {
         if (bad) atomicCAS((int *)&P.hdr->err, 0, ERR_OFFSETS);
         P.hdr->nchunks = (uint32_t)nch;
+        P.hdr->k1 = (uint32_t)k1;
         P.hdr->sel = tagged ? 1 : 0;
         P.hdr->ssel = (double)(offR - off0) < (double)P.short_len * (double)P.R ? 1 : 0;
         P.hdr->base0 = base0;
@@ -162,7 +190,7 @@ __global__ void k_prepass(KParams P) {
         if (k == nch) {
             fr = (uint32_t)P.R;
         } else {
-            long long b = (k == 0) ? off0 : base0 + k * (long long)P.C;
+            long long b = (k == 0) ? off0 : chunk_start(base0, k, C, k1);
             long long lo = 0, hi = P.R;  // first r in [0,R) with off[r] >= b, else R
             while (lo < hi) {
                 long long mid = (lo + hi) >> 1;
@@ -189,19 +217,19 @@ __global__ void k_fixup(KParams P) {
     using AT = AggT<AGG>;
     const WsHdr *H = P.hdr;
     const long long nch = H->nchunks;
-    const long long base0 = H->base0, offR = H->offR;
+    const long long base0 = H->base0, offR = H->offR, k1 = H->k1;
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k + 1 < nch;
          k += (long long)gridDim.x * blockDim.x) {
         uint32_t f0 = P.chunk_fr[k], f1 = P.chunk_fr[k + 1];
         if (f1 <= f0) continue;                       // no region starts in chunk k
         long long r = (long long)f1 - 1;               // last region starting in chunk k
-        long long end_k = base0 + (k + 1) * (long long)P.C;
+        long long end_k = chunk_start(base0, k + 1, P.C, k1);
         long long rend = P.off[r + 1];
         if (rend <= end_k) continue;                   // not split
         typename AT::A acc = AT::load(P.part0, P.part1, (uint64_t)(2 * k + 1));
         for (long long j = k + 1; j < nch; ++j) {
             acc = AT::comb(acc, AT::load(P.part0, P.part1, (uint64_t)(2 * j)));
-            long long end_j = base0 + (j + 1) * (long long)P.C;
+            long long end_j = chunk_start(base0, j + 1, P.C, k1);
             if (end_j > offR) end_j = offR;
             if (rend <= end_j) break;
         }

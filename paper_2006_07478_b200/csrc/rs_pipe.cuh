@@ -682,8 +682,9 @@ struct Pipe {
     // ---------------------------------------------------------- chunks
     __device__ __forceinline__ void load_chunk(Chunk &c, int32_t k, uint32_t pos) const {
         c.k = k;
-        c.beg = (k == 0) ? off0 : base0 + (long long)k * P.C;
-        long long e = base0 + (long long)(k + 1) * P.C;
+        const long long k1 = P.hdr->k1;
+        c.beg = (k == 0) ? off0 : chunk_start(base0, k, P.C, k1);
+        long long e = chunk_start(base0, k + 1, P.C, k1);
         c.end = e > offR ? offR : e;
         c.pos = pos;
         c.fr0 = P.chunk_fr[k];

@@ -125,8 +125,9 @@ def test_auto_strategy_host_side(rs):
     import synth
     p = rs.Pipeline(synth.sweep_stages(3), "sum_i64", strategy="auto")
     assert p.last_strategy() == "auto"
-    s = rs.Pipeline(synth.sweep_stages(3), "sum_i64", strategy="signal")
-    t = rs.Pipeline(synth.sweep_stages(3), "sum_i64", strategy="tagged")
+    # (AUTO's two kernels share one chunk table of 8192-child chunks)
+    s = rs.Pipeline(synth.sweep_stages(3), "sum_i64", strategy="signal", chunk=8192)
+    t = rs.Pipeline(synth.sweep_stages(3), "sum_i64", strategy="tagged", chunk=8192)
     for R, N in ((10, 1000), (1 << 20, 1 << 24)):
         assert p.workspace_bytes(R, N) == max(s.workspace_bytes(R, N), t.workspace_bytes(R, N))
     assert s.last_strategy() == "signal" and t.last_strategy() == "tagged"

@@ -71,7 +71,7 @@ def assert_parity(got, ref, agg):
 def test_tiny_d1(rs, strategy):
     vals, off, stages, agg = synth.tiny()
     ref = oracle.brute(vals, off, stages, agg)
-    got, st, _ = run_gpu(rs, vals, off, stages, agg, strategy)
+    got, st, _ = run_gpu(rs, vals, off, stages, agg, strategy, chunk=8192)   # uniform chunks (no finer tail)
     assert_parity(got, ref, agg)
     kc = oracle.node_counts(vals, off, stages)
     assert st[0][2] == off[-1] - off[0]                      # enumerated children = sum of sizes
@@ -80,7 +80,7 @@ def test_tiny_d1(rs, strategy):
     if strategy == "signal":
         # Begin + End per region part: regions crossing a chunk boundary are
         # split into one part per chunk they touch (A18)
-        C = rs.Pipeline(stages, agg).geometry()["chunk"] or 8192
+        C = 8192
         b = np.arange(C, int(off[-1]), C)
         splits = sum(int(((off[:-1] < x) & (off[1:] > x)).sum()) for x in b)
         assert st[0][3] == 2 * (off.size - 1 + splits)
