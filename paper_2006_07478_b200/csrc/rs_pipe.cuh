@@ -989,11 +989,25 @@ struct Pipe {
             return;
         }
         const uint32_t excl = cum - cnt;
-        const uint32_t maxc = __reduce_max_sync(kFull, lane < m ? cnt : 0u);
-        if (maxc <= 4) {
-            // short parts: lane i writes part i's few tags directly
-            for (uint32_t r = 0; r < maxc; ++r)
-                if (lane < m && r < cnt) T<0>()[(E<0>().qt + excl + r) & (ring0 - 1)] = key;
+        // Lane i writes short part i's tags itself (<= 8 items) and the warp writes
+        // each longer part 32 tags at a time -- when the long parts average 64
+        // items or more (Zipf-like mixes, U{0..2L} with L >= 64).  Otherwise
+        // (many parts of a few dozen items) every item finds its part by a
+        // binary search over the parts' starts.
+        const bool lng = (uint32_t)lane < m && cnt > 8u;
+        uint32_t lg = __ballot_sync(kFull, lng);
+        if (tot >= 64u * __popc(lg)) {
+            const uint32_t maxs = __reduce_max_sync(kFull, ((uint32_t)lane < m && !lng) ? cnt : 0u);
+#pragma unroll 1
+            for (uint32_t r = 0; r < maxs; ++r)
+                if ((uint32_t)lane < m && !lng && r < cnt) T<0>()[(E<0>().qt + excl + r) & (ring0 - 1)] = key;
+#pragma unroll 1
+            while (lg) {
+                const uint32_t j = __ffs(lg) - 1;
+                lg &= lg - 1u;
+                const uint32_t x = __shfl_sync(kFull, excl, j), c = __shfl_sync(kFull, cnt, j), k = __shfl_sync(kFull, key, j);
+                for (uint32_t i = lane; i < c; i += 32) T<0>()[(E<0>().qt + x + i) & (ring0 - 1)] = k;
+            }
             return;
         }
         for (uint32_t base = 0; base < tot; base += 32) {
