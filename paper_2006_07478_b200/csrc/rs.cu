@@ -139,7 +139,8 @@ WsLayout layout(const rs_pipeline *p, long long n_regions, long long n_elems, co
     w.max_chunks = (n_elems + 16) / C + 2;
     // the last round in pieces of C >> TAIL_SH: at most 2^TAIL_SH (instances + 1) more chunks
     // (instances <= 4095 covered; the prepass keeps uniform chunks when they would not fit)
-    if (p->chunk_tail) w.max_chunks += (1ll << TAIL_SH) * 4096;
+    if (p->chunk_tail)
+        w.max_chunks += std::min<long long>((1ll << TAIL_SH) * 4096, (n_elems + 16) / (C >> TAIL_SH) + 1);
     w.hdr = 0;
     w.stats = 256;
     w.fr = w.stats + align256(sizeof(unsigned long long) * (4 * (MAXK + 2) + 16));
