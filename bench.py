@@ -730,8 +730,10 @@ def run_sweep(rs, torch, dev, args):
                 e.update({"dist": dist_, "L": L, "sawtooth": L not in Ls})
                 if strat == "signal":
                     e["bound"] = bound
-                    # the prepass's rule (rs.h RS_FLAG_SHORT_ON): short-region kernel below 96 children/region
-                    e["kernel"] = "short-region" if e["children"] < 96 * e["regions"] else "general"
+                    # the prepass's rule (rs.h RS_FLAG_SHORT_ON): short-region kernel below 96 children per
+                    # region, or below 176 when the regions are of equal length
+                    mean = e["children"] / e["regions"]
+                    e["kernel"] = "short-region" if mean < 96 or (dist_ == "fixed" and mean < 176) else "general"
                 res.append(e)
             if L in Ls and L < 96:             # the general signal kernel at the same point
                 e = _time_point(rs, torch, dev, args, vals, off, stages3, "sum_i64", "signal", rs.RS_FLAG_SHORT_OFF)

@@ -161,8 +161,9 @@ enum {
                                 regions shorter than w.  Default (neither flag):
                                 when n_elems < 2w * n_regions both kernels are enqueued and the
                                 prepass picks the short-region one iff the call's children
-                                off[R] - off[0] < 96 * R (decided on the device, like AUTO;
-                                the crossover measured on B200).  Its default geometry is its
+                                off[R] - off[0] < 96 * R, or < 176 * R when 64 sampled region
+                                lengths are within 1/8 of the mean (decided on the device, like
+                                AUTO; the crossovers measured on B200).  Its default geometry is its
                                 own (a 16w ring, stages of 4w, signal queues of 128) unless
                                 queue_cap / signal_cap / q0_stage are set. */
     RS_FLAG_UNFUSED = 32u    /* sequential scheduler: keep the AGGREGATE as a separate node

@@ -180,7 +180,23 @@ __global__ void k_prepass(KParams P) {
         P.hdr->nchunks = (uint32_t)nch;
         P.hdr->k1 = (uint32_t)k1;
         P.hdr->sel = tagged ? 1 : 0;
-        P.hdr->ssel = (double)(offR - off0) < (double)P.short_len * (double)P.R ? 1 : 0;
+        bool shrt = (double)(offR - off0) < (double)P.short_len * (double)P.R;
+        // equal-length regions below 176 children (the sawtooth around w): the
+        // short-region kernel still wins there (its segments after the first stage
+        // are below w), variable lengths of that mean do not -- 64 sampled lengths
+        // within 1/8 of the mean count as equal
+        if (P.short_len && !shrt && (double)(offR - off0) < 176.0 * (double)P.R) {
+            const double mean = (double)(offR - off0) / (double)P.R;
+            long long lo = offR - off0, hi = 0;
+            for (int i = 0; i < 64; ++i) {
+                const long long r = (long long)i * P.R / 64;
+                const long long len = P.off[r + 1] - P.off[r];
+                lo = len < lo ? len : lo;
+                hi = len > hi ? len : hi;
+            }
+            shrt = (double)(hi - lo) <= mean / 8.0;
+        }
+        P.hdr->ssel = shrt ? 1 : 0;
         P.hdr->base0 = base0;
         P.hdr->off0 = off0;
         P.hdr->offR = offR;
